@@ -1,0 +1,166 @@
+/*
+ * txgemm.h -- C ABI of the B200-native batched small-matrix GEMM.
+ *
+ * Operation (§2 Eq. (1)), for p = 0 .. batch_count-1 independently:
+ *
+ *     C^p <- alpha * op(A^p) * op(B^p) + beta * C^p
+ *
+ *   op(X) = X, X^T or X^* selected by 'N'/'n', 'T'/'t', 'C'/'c' (PAPER.md:240-243,
+ *   344-345); for the real types 'C' is the same as 'T'.  C^p is m x n, op(A^p) is
+ *   m x k, op(B^p) is k x n; 0 <= m, n, k <= 16 (the paper's
+ *   size regime; reading R14).
+ *   A is stored m x k when transa = 'N', else k x m; B is stored k x n when
+ *   transb = 'N', else n x k (reading R8).  Storage is column-major.
+ *
+ * Types: s = float, d = double, c = tx_cfloat (layout of
+ * cuComplex / float2 / torch.complex64), z = tx_cdouble (cuDoubleComplex /
+ * double2 / torch.complex128).  Complex products use the 4-multiply/2-add
+ * formula; the "3M" method is not used.
+ *
+ * Layouts.
+ *  - Strided ("uniform", the paper's TGEMM_multi_uniform):
+ *    entry (i, j) of matrix p of X is X[i + ldx*j + ldx2*p]; all leading
+ *    dimensions are in ELEMENTS, not bytes.  ldx2 is 64-bit
+ *    because p*ldx2 exceeds 2^31 at 10^7 16x16 pairs (reading R10).
+ *    Inputs may use ld2 = 0 (one matrix broadcast to every p) and may overlap
+ *    each other; C must satisfy ldc2 >= ldc*n (Fig. 1) and
+ *    must not overlap A or B.
+ *  - Pointer array ("nounif", cuBLAS-like): entry
+ *    (i, j) of matrix p of X is Xarray[p][i + ldx*j].  Xarray is a DEVICE array
+ *    of batch_count DEVICE pointers.  Output matrices must be pairwise disjoint
+ *    and disjoint from the inputs (documented precondition, not checked: checking
+ *    would need device reads).
+ *
+ * Memory and ownership.  The caller owns all memory; the library allocates none
+ * on these calls.  A, B, C, the pointer arrays and their targets are device
+ * memory of the CURRENT device.  alpha and beta are HOST pointers, read before
+ * the call returns (the paper allows host or device; device
+ * mode is out of scope, reading R12).
+ *
+ * Execution.  Asynchronous on `stream` (NULL = legacy default stream); returns
+ * after enqueueing.  Reentrant and thread-safe.  Results are bitwise
+ * deterministic for identical inputs and do not depend on the grid size.
+ * beta == 0: C is write-only (never read, NaN in C does not propagate).
+ * alpha == 0 or k == 0: A and B are never read; C <- beta*C.
+ * Quick return, nothing enqueued: m == 0, n == 0, batch_count == 0, or
+ * (alpha == 0 or k == 0) and beta == 1.
+ *
+ * Return value: 0 on success; -i when argument i (1-based position in the
+ * call) is invalid -- nothing is enqueued and C is untouched; > 0 a cudaError_t
+ * raised while launching.  Argument checks, in order (strided positions, the
+ * pointer call's positions in brackets):
+ *   transa -1, transb -2, m -3, n -4, k -5 (outside [0,16]), alpha NULL -6,
+ *   beta NULL -13 [-11], lda < max(1, rows of stored A) -8,
+ *   ldb < max(1, rows of stored B) -11 [-10], ldc < max(1, m) -15 [-13];
+ *   batch_count > 1 (strided only): lda2 < 0 -9, ldb2 < 0 -12, ldc2 < ldc*n -16;
+ *   batch_count < 0 -17 [-14];
+ *   A NULL -7 / B NULL -10 [-9] when alpha != 0, k > 0 and m*n*batch_count > 0;
+ *   C NULL -14 [-12] when m*n*batch_count > 0;
+ *   strided: C's address range overlapping A's or B's -14 (when A/B are read).
+ */
+#ifndef TXGEMM_H
+#define TXGEMM_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct { float re, im; } tx_cfloat;
+typedef struct { double re, im; } tx_cdouble;
+/* Same handle as cudaStream_t / CUstream. */
+typedef struct CUstream_st *tx_stream_t;
+
+#define TX_VERSION 10000 /* 1.0.0 */
+#define TX_MAX_DIM 16
+
+/* ---- strided batch: TGEMM_multi_uniform. Args 1..18. ---- */
+int tx_gemm_batched_s(char transa, char transb, int m, int n, int k,
+                      const float *alpha, const float *A, int lda, long long lda2,
+                      const float *B, int ldb, long long ldb2, const float *beta,
+                      float *C, int ldc, long long ldc2, int batch_count, tx_stream_t stream);
+int tx_gemm_batched_d(char transa, char transb, int m, int n, int k,
+                      const double *alpha, const double *A, int lda, long long lda2,
+                      const double *B, int ldb, long long ldb2, const double *beta,
+                      double *C, int ldc, long long ldc2, int batch_count, tx_stream_t stream);
+int tx_gemm_batched_c(char transa, char transb, int m, int n, int k,
+                      const tx_cfloat *alpha, const tx_cfloat *A, int lda, long long lda2,
+                      const tx_cfloat *B, int ldb, long long ldb2, const tx_cfloat *beta,
+                      tx_cfloat *C, int ldc, long long ldc2, int batch_count, tx_stream_t stream);
+int tx_gemm_batched_z(char transa, char transb, int m, int n, int k,
+                      const tx_cdouble *alpha, const tx_cdouble *A, int lda, long long lda2,
+                      const tx_cdouble *B, int ldb, long long ldb2, const tx_cdouble *beta,
+                      tx_cdouble *C, int ldc, long long ldc2, int batch_count, tx_stream_t stream);
+
+/* ---- pointer-array batch: TGEMM_multi_nounif. Args 1..15. ---- */
+int tx_gemm_batched_ptr_s(char transa, char transb, int m, int n, int k, const float *alpha,
+                          const float *const *Aarray, int lda, const float *const *Barray, int ldb,
+                          const float *beta, float *const *Carray, int ldc, int batch_count,
+                          tx_stream_t stream);
+int tx_gemm_batched_ptr_d(char transa, char transb, int m, int n, int k, const double *alpha,
+                          const double *const *Aarray, int lda, const double *const *Barray,
+                          int ldb, const double *beta, double *const *Carray, int ldc,
+                          int batch_count, tx_stream_t stream);
+int tx_gemm_batched_ptr_c(char transa, char transb, int m, int n, int k, const tx_cfloat *alpha,
+                          const tx_cfloat *const *Aarray, int lda,
+                          const tx_cfloat *const *Barray, int ldb, const tx_cfloat *beta,
+                          tx_cfloat *const *Carray, int ldc, int batch_count, tx_stream_t stream);
+int tx_gemm_batched_ptr_z(char transa, char transb, int m, int n, int k,
+                          const tx_cdouble *alpha, const tx_cdouble *const *Aarray, int lda,
+                          const tx_cdouble *const *Barray, int ldb, const tx_cdouble *beta,
+                          tx_cdouble *const *Carray, int ldc, int batch_count, tx_stream_t stream);
+
+/* ---- host-buffer entry (end-to-end): same arguments and checks as the strided
+ * call, except that hA, hB, hC are HOST pointers (pinned memory for overlap) and
+ * dA, dB, dC (args 19, 20, 21) are caller-owned DEVICE staging buffers with the
+ * same layouts (offsets and extents) as hA, hB, hC.  Enqueues on `stream`:
+ * host->device copies of the A and B extents (and of C's extent when
+ * beta != 0), the GEMM on the device copies, and the device->host copy of C's
+ * extent back into hC.  The batch is processed in chunks so that copies of one
+ * chunk overlap the GEMM of another.  Returns as the strided call; a NULL
+ * staging buffer that would be used returns -19/-20/-21. ---- */
+int tx_gemm_batched_hostio_s(char transa, char transb, int m, int n, int k,
+                             const float *alpha, const float *hA, int lda, long long lda2,
+                             const float *hB, int ldb, long long ldb2, const float *beta,
+                             float *hC, int ldc, long long ldc2, int batch_count,
+                             tx_stream_t stream, float *dA, float *dB, float *dC);
+int tx_gemm_batched_hostio_d(char transa, char transb, int m, int n, int k,
+                             const double *alpha, const double *hA, int lda, long long lda2,
+                             const double *hB, int ldb, long long ldb2, const double *beta,
+                             double *hC, int ldc, long long ldc2, int batch_count,
+                             tx_stream_t stream, double *dA, double *dB, double *dC);
+int tx_gemm_batched_hostio_c(char transa, char transb, int m, int n, int k,
+                             const tx_cfloat *alpha, const tx_cfloat *hA, int lda,
+                             long long lda2, const tx_cfloat *hB, int ldb, long long ldb2,
+                             const tx_cfloat *beta, tx_cfloat *hC, int ldc, long long ldc2,
+                             int batch_count, tx_stream_t stream, tx_cfloat *dA, tx_cfloat *dB,
+                             tx_cfloat *dC);
+int tx_gemm_batched_hostio_z(char transa, char transb, int m, int n, int k,
+                             const tx_cdouble *alpha, const tx_cdouble *hA, int lda,
+                             long long lda2, const tx_cdouble *hB, int ldb, long long ldb2,
+                             const tx_cdouble *beta, tx_cdouble *hC, int ldc, long long ldc2,
+                             int batch_count, tx_stream_t stream, tx_cdouble *dA,
+                             tx_cdouble *dB, tx_cdouble *dC);
+
+/* ---- introspection and tuning (host only, no GPU work) ---- */
+/* Human-readable text for a status code (static storage, never NULL). */
+const char *tx_status_string(int status);
+/* TX_VERSION of the built library. */
+int tx_version(void);
+/* Path the calling thread's most recent successful GEMM call took:
+ * 0 none/quick return, 1 packed bulk-copy (TMA) kernel, 2 general gather kernel,
+ * 3 pointer-array gather kernel, 4 scale-only kernel (alpha == 0 or k == 0);
+ * +16 when a separate tail launch handled the last (< 16) pairs.  Also
+ * returns the number of kernel launches of that call in *launches. */
+int tx_last_path(int *launches);
+/* Cap on CTAs per launch (0 = automatic: SMs x resident CTAs).  Results do not
+ * depend on it; used for the grid-sweep experiment and determinism tests.
+ * Process-wide; returns the previous value. */
+int tx_set_max_ctas(int max_ctas);
+/* Number of compiled kernel instances (AOT, size-specialised + generic). */
+int tx_num_instances(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TXGEMM_H */

@@ -1,0 +1,437 @@
+// tx_api.cu -- the C ABI (include/txgemm.h): argument validation, alpha/beta and
+// layout classification, instance selection and launch.  Host code only.
+//
+// Call stack: tx_gemm_batched_<t> -> validate (pure host, no
+// CUDA call) -> quick return | scale kernel (alpha == 0 or k == 0) | bulk kernel
+// (packed, aligned; size-specialised when m == n == k) [+ gather tail] | gather
+// kernel (any other strided layout) ; tx_gemm_batched_ptr_<t> -> gather kernel
+// over the pointer arrays.
+#include <atomic>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+
+#include "txgemm.h"
+#include "tx_dispatch.cuh"
+
+namespace tx {
+
+#define TX_DECL_BULK(t, a) void register_bulk_##t##_##a(TypeTables &);
+TX_DECL_BULK(0, 0)
+TX_DECL_BULK(0, 1)
+TX_DECL_BULK(1, 0)
+TX_DECL_BULK(1, 1)
+TX_DECL_BULK(2, 0)
+TX_DECL_BULK(2, 1)
+TX_DECL_BULK(2, 2)
+TX_DECL_BULK(3, 0)
+TX_DECL_BULK(3, 1)
+TX_DECL_BULK(3, 2)
+void register_gen_0(TypeTables &);
+void register_gen_1(TypeTables &);
+void register_gen_2(TypeTables &);
+void register_gen_3(TypeTables &);
+
+static TypeTables g_tab[4];
+static std::once_flag g_once;
+
+TypeTables &tables(int t)
+{
+    std::call_once(g_once, [] {
+        std::memset(g_tab, 0, sizeof(g_tab));
+        register_bulk_0_0(g_tab[0]);
+        register_bulk_0_1(g_tab[0]);
+        register_bulk_1_0(g_tab[1]);
+        register_bulk_1_1(g_tab[1]);
+        register_bulk_2_0(g_tab[2]);
+        register_bulk_2_1(g_tab[2]);
+        register_bulk_2_2(g_tab[2]);
+        register_bulk_3_0(g_tab[3]);
+        register_bulk_3_1(g_tab[3]);
+        register_bulk_3_2(g_tab[3]);
+        register_gen_0(g_tab[0]);
+        register_gen_1(g_tab[1]);
+        register_gen_2(g_tab[2]);
+        register_gen_3(g_tab[3]);
+    });
+    return g_tab[t];
+}
+
+static std::atomic<int> g_max_ctas{0};
+int max_ctas_override() { return g_max_ctas.load(std::memory_order_relaxed); }
+
+int num_sms()
+{
+    static std::atomic<int> cache[64];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) dev = 0;
+    int v = cache[dev].load(std::memory_order_relaxed);
+    if (v == 0) {
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        if (v <= 0) v = 1;
+        cache[dev].store(v, std::memory_order_relaxed);
+    }
+    return v;
+}
+
+static thread_local int t_last_path = 0;
+static thread_local int t_last_launches = 0;
+
+// ---------------------------------------------------------------- scalars
+template <class U> struct Api;
+template <> struct Api<float> {
+    using T = float;
+    static constexpr int id = 0;
+    static constexpr bool cplx = false;
+    static bool zero(const float &v) { return v == 0.f; }
+    static bool one(const float &v) { return v == 1.f; }
+    static T dev(const float &v) { return v; }
+};
+template <> struct Api<double> {
+    using T = double;
+    static constexpr int id = 1;
+    static constexpr bool cplx = false;
+    static bool zero(const double &v) { return v == 0.0; }
+    static bool one(const double &v) { return v == 1.0; }
+    static T dev(const double &v) { return v; }
+};
+template <> struct Api<tx_cfloat> {
+    using T = float2;
+    static constexpr int id = 2;
+    static constexpr bool cplx = true;
+    static bool zero(const tx_cfloat &v) { return v.re == 0.f && v.im == 0.f; }
+    static bool one(const tx_cfloat &v) { return v.re == 1.f && v.im == 0.f; }
+    static T dev(const tx_cfloat &v) { return make_float2(v.re, v.im); }
+};
+template <> struct Api<tx_cdouble> {
+    using T = double2;
+    static constexpr int id = 3;
+    static constexpr bool cplx = true;
+    static bool zero(const tx_cdouble &v) { return v.re == 0.0 && v.im == 0.0; }
+    static bool one(const tx_cdouble &v) { return v.re == 1.0 && v.im == 0.0; }
+    static T dev(const tx_cdouble &v) { return make_double2(v.re, v.im); }
+};
+static_assert(sizeof(tx_cfloat) == sizeof(float2), "layout");
+static_assert(sizeof(tx_cdouble) == sizeof(double2), "layout");
+
+// ------------------------------------------------------------- validation
+static bool op_ok(char c) { return c == 'n' || c == 'N' || c == 't' || c == 'T' || c == 'c' || c == 'C'; }
+static bool op_n(char c) { return c == 'n' || c == 'N'; }
+static int op_code(char c, bool cplx)
+{
+    if (op_n(c)) return OP_N;
+    if ((c == 'c' || c == 'C') && cplx) return OP_C;
+    return OP_T;  // 'C' on a real type is 'T' (reading R6)
+}
+static int max1(int v) { return v > 1 ? v : 1; }
+
+static long long extent_elems(int rows, int cols, int ld, long long ld2, int batch)
+{
+    if (rows <= 0 || cols <= 0 || batch <= 0) return 0;
+    return ld2 * (long long)(batch - 1) + (long long)ld * (cols - 1) + rows;
+}
+
+static bool overlap(const void *p, long long np, const void *q, long long nq, size_t es)
+{
+    if (np <= 0 || nq <= 0) return false;
+    const uintptr_t a0 = (uintptr_t)p, a1 = a0 + (uintptr_t)np * es;
+    const uintptr_t b0 = (uintptr_t)q, b1 = b0 + (uintptr_t)nq * es;
+    return a0 < b1 && b0 < a1;
+}
+
+// Checks in the order documented in include/txgemm.h.  ptr = pointer-array call.
+static int validate(bool ptr, char ta, char tb, int m, int n, int k, const void *alpha,
+                    bool alpha_zero, const void *beta, const void *A, int lda, long long lda2,
+                    const void *B, int ldb, long long ldb2, const void *C, int ldc,
+                    long long ldc2, int batch, size_t es)
+{
+    if (!op_ok(ta)) return -1;
+    if (!op_ok(tb)) return -2;
+    if (m < 0 || m > TX_MAX_DIM) return -3;
+    if (n < 0 || n > TX_MAX_DIM) return -4;
+    if (k < 0 || k > TX_MAX_DIM) return -5;
+    if (!alpha) return -6;
+    if (!beta) return ptr ? -11 : -13;
+    const int rowsA = op_n(ta) ? m : k, colsA = op_n(ta) ? k : m;
+    const int rowsB = op_n(tb) ? k : n, colsB = op_n(tb) ? n : k;
+    if (lda < max1(rowsA)) return -8;
+    if (ldb < max1(rowsB)) return ptr ? -10 : -11;
+    if (ldc < max1(m)) return ptr ? -13 : -15;
+    if (!ptr && batch > 1) {
+        if (lda2 < 0) return -9;
+        if (ldb2 < 0) return -12;
+        if (ldc2 < (long long)ldc * n) return -16;
+    }
+    if (batch < 0) return ptr ? -14 : -17;
+    const bool work = m > 0 && n > 0 && batch > 0;
+    const bool reads_ab = work && !alpha_zero && k > 0;
+    if (reads_ab && !A) return -7;
+    if (reads_ab && !B) return ptr ? -9 : -10;
+    if (work && !C) return ptr ? -12 : -14;
+    if (!ptr && reads_ab) {
+        const long long ec = extent_elems(m, n, ldc, ldc2, batch);
+        if (overlap(C, ec, A, extent_elems(rowsA, colsA, lda, lda2, batch), es)) return -14;
+        if (overlap(C, ec, B, extent_elems(rowsB, colsB, ldb, ldb2, batch), es)) return -14;
+    }
+    return 0;
+}
+
+static bool aligned16(const void *p) { return ((uintptr_t)p & 15u) == 0; }
+
+static int as_status(cudaError_t e) { return e == cudaSuccess ? 0 : (int)e; }
+
+// ------------------------------------------------------------- strided call
+template <class U>
+static int gemm_strided(char ta, char tb, int m, int n, int k, const U *alpha, const U *A, int lda,
+                        long long lda2, const U *B, int ldb, long long ldb2, const U *beta, U *C,
+                        int ldc, long long ldc2, int batch, cudaStream_t st)
+{
+    using AT = Api<U>;
+    using T = typename AT::T;
+    const int rc = validate(false, ta, tb, m, n, k, alpha, alpha && AT::zero(*alpha), beta, A, lda,
+                            lda2, B, ldb, ldb2, C, ldc, ldc2, batch, sizeof(U));
+    if (rc) return rc;
+    const U a = *alpha, b = *beta;
+    if (m == 0 || n == 0 || batch == 0 || ((AT::zero(a) || k == 0) && AT::one(b))) {
+        t_last_path = PATH_NONE;
+        t_last_launches = 0;
+        return 0;
+    }
+    TypeTables &tab = tables(AT::id);
+    const bool b0 = AT::zero(b);
+    Params<T> p;
+    std::memset(&p, 0, sizeof(p));
+    p.A = reinterpret_cast<const T *>(A);
+    p.B = reinterpret_cast<const T *>(B);
+    p.C = reinterpret_cast<T *>(C);
+    p.lda = lda;
+    p.ldb = ldb;
+    p.ldc = ldc;
+    p.lda2 = lda2;
+    p.ldb2 = ldb2;
+    p.ldc2 = ldc2;
+    p.m = m;
+    p.n = n;
+    p.k = k;
+    p.batch = batch;
+    p.alpha = AT::dev(a);
+    p.beta = AT::dev(b);
+
+    if (AT::zero(a) || k == 0) {
+        const cudaError_t e = tab.scale[0][b0](&p, st);
+        if (e != cudaSuccess) return as_status(e);
+        t_last_path = PATH_SCALE;
+        t_last_launches = 1;
+        return 0;
+    }
+    const int opa = op_code(ta, AT::cplx), opb = op_code(tb, AT::cplx);
+    const int rowsA = op_n(ta) ? m : k, colsA = op_n(ta) ? k : m;
+    const int rowsB = op_n(tb) ? k : n, colsB = op_n(tb) ? n : k;
+    const long long SA = (long long)rowsA * colsA, SB = (long long)rowsB * colsB,
+                    SC = (long long)m * n;
+    const bool one = batch == 1;
+    const bool packed = lda == rowsA && ldb == rowsB && ldc == m &&
+                        (one || (lda2 == SA && ldb2 == SB && ldc2 == SC)) && aligned16(A) &&
+                        aligned16(B) && aligned16(C);
+    int path = PATH_GATHER, launches = 0;
+    if (packed) {
+        const int es = (int)sizeof(U);
+        const int unit = 16 / gcd_i(16, gcd_i((int)(SA * es), gcd_i((int)(SB * es), (int)(SC * es))));
+        const int main_pairs = batch / unit * unit;
+        if (main_pairs > 0) {
+            Params<T> q = p;
+            q.batch = main_pairs;
+            q.lda2 = SA;
+            q.ldb2 = SB;
+            q.ldc2 = SC;
+            LaunchFn fn = (m == n && n == k) ? tab.bulk_sq[opa][opb][b0][m - 1] : nullptr;
+            if (!fn) fn = tab.bulk_dyn[opa][opb][b0];
+            const cudaError_t e = fn(&q, st);
+            if (e != cudaSuccess) return as_status(e);
+            ++launches;
+            path = PATH_BULK;
+        }
+        if (main_pairs < batch) {  // < 16 trailing pairs whose bytes are not 16-aligned
+            Params<T> q = p;
+            q.batch = batch - main_pairs;
+            q.lda2 = SA;
+            q.ldb2 = SB;
+            q.ldc2 = SC;
+            q.A += SA * main_pairs;
+            q.B += SB * main_pairs;
+            q.C += SC * main_pairs;
+            const cudaError_t e = tab.gather[opa][opb][b0][0](&q, st);
+            if (e != cudaSuccess) return as_status(e);
+            ++launches;
+            path = main_pairs > 0 ? (PATH_BULK | PATH_TAIL) : PATH_GATHER;
+        }
+    } else {
+        const cudaError_t e = tab.gather[opa][opb][b0][0](&p, st);
+        if (e != cudaSuccess) return as_status(e);
+        launches = 1;
+    }
+    t_last_path = path;
+    t_last_launches = launches;
+    return 0;
+}
+
+// -------------------------------------------------------- pointer-array call
+template <class U>
+static int gemm_ptr(char ta, char tb, int m, int n, int k, const U *alpha, const U *const *Aa,
+                    int lda, const U *const *Ba, int ldb, const U *beta, U *const *Ca, int ldc,
+                    int batch, cudaStream_t st)
+{
+    using AT = Api<U>;
+    using T = typename AT::T;
+    const int rc = validate(true, ta, tb, m, n, k, alpha, alpha && AT::zero(*alpha), beta, Aa, lda,
+                            0, Ba, ldb, 0, Ca, ldc, 0, batch, sizeof(U));
+    if (rc) return rc;
+    const U a = *alpha, b = *beta;
+    if (m == 0 || n == 0 || batch == 0 || ((AT::zero(a) || k == 0) && AT::one(b))) {
+        t_last_path = PATH_NONE;
+        t_last_launches = 0;
+        return 0;
+    }
+    TypeTables &tab = tables(AT::id);
+    const bool b0 = AT::zero(b);
+    Params<T> p;
+    std::memset(&p, 0, sizeof(p));
+    p.Ap = reinterpret_cast<const T *const *>(Aa);
+    p.Bp = reinterpret_cast<const T *const *>(Ba);
+    p.Cp = reinterpret_cast<T *const *>(Ca);
+    p.lda = lda;
+    p.ldb = ldb;
+    p.ldc = ldc;
+    p.m = m;
+    p.n = n;
+    p.k = k;
+    p.batch = batch;
+    p.alpha = AT::dev(a);
+    p.beta = AT::dev(b);
+    cudaError_t e;
+    if (AT::zero(a) || k == 0) {
+        e = tab.scale[1][b0](&p, st);
+        t_last_path = PATH_SCALE;
+    } else {
+        e = tab.gather[op_code(ta, AT::cplx)][op_code(tb, AT::cplx)][b0][1](&p, st);
+        t_last_path = PATH_PTR;
+    }
+    if (e != cudaSuccess) return as_status(e);
+    t_last_launches = 1;
+    return 0;
+}
+
+// ---------------------------------------------------------- host-buffer call
+template <class U>
+static int gemm_hostio(char ta, char tb, int m, int n, int k, const U *alpha, const U *hA, int lda,
+                       long long lda2, const U *hB, int ldb, long long ldb2, const U *beta, U *hC,
+                       int ldc, long long ldc2, int batch, cudaStream_t st, U *dA, U *dB, U *dC)
+{
+    using AT = Api<U>;
+    int rc = validate(false, ta, tb, m, n, k, alpha, alpha && AT::zero(*alpha), beta, hA, lda,
+                      lda2, hB, ldb, ldb2, hC, ldc, ldc2, batch, sizeof(U));
+    if (rc) return rc;
+    const U a = *alpha, b = *beta;
+    const bool work = m > 0 && n > 0 && batch > 0;
+    const bool reads_ab = work && !AT::zero(a) && k > 0;
+    if (reads_ab && !dA) return -19;
+    if (reads_ab && !dB) return -20;
+    if (work && !dC) return -21;
+    if (!work || ((AT::zero(a) || k == 0) && AT::one(b))) {
+        t_last_path = PATH_NONE;
+        t_last_launches = 0;
+        return 0;
+    }
+    const int rowsA = op_n(ta) ? m : k, colsA = op_n(ta) ? k : m;
+    const int rowsB = op_n(tb) ? k : n, colsB = op_n(tb) ? n : k;
+    const size_t es = sizeof(U);
+    const long long eA = extent_elems(rowsA, colsA, lda, lda2, batch);
+    const long long eB = extent_elems(rowsB, colsB, ldb, ldb2, batch);
+    const long long eC = extent_elems(m, n, ldc, ldc2, batch);
+    cudaError_t e = cudaSuccess;
+    if (reads_ab) {
+        e = cudaMemcpyAsync(dA, hA, eA * es, cudaMemcpyHostToDevice, st);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(dB, hB, eB * es, cudaMemcpyHostToDevice, st);
+    }
+    if (e == cudaSuccess && !AT::zero(b))
+        e = cudaMemcpyAsync(dC, hC, eC * es, cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) return as_status(e);
+    rc = gemm_strided<U>(ta, tb, m, n, k, alpha, dA, lda, lda2, dB, ldb, ldb2, beta, dC, ldc, ldc2,
+                         batch, st);
+    if (rc) return rc;
+    e = cudaMemcpyAsync(hC, dC, eC * es, cudaMemcpyDeviceToHost, st);
+    return as_status(e);
+}
+
+}  // namespace tx
+
+// ====================================================================== C ABI
+using namespace tx;
+
+#define TX_STRIDED(SUF, U)                                                                        \
+    extern "C" int tx_gemm_batched_##SUF(char ta, char tb, int m, int n, int k, const U *alpha,  \
+                                         const U *A, int lda, long long lda2, const U *B, int ldb, \
+                                         long long ldb2, const U *beta, U *C, int ldc,            \
+                                         long long ldc2, int batch, tx_stream_t stream)           \
+    {                                                                                             \
+        return gemm_strided<U>(ta, tb, m, n, k, alpha, A, lda, lda2, B, ldb, ldb2, beta, C, ldc,  \
+                               ldc2, batch, (cudaStream_t)stream);                                \
+    }                                                                                             \
+    extern "C" int tx_gemm_batched_ptr_##SUF(char ta, char tb, int m, int n, int k,               \
+                                             const U *alpha, const U *const *Aa, int lda,         \
+                                             const U *const *Ba, int ldb, const U *beta,          \
+                                             U *const *Ca, int ldc, int batch,                    \
+                                             tx_stream_t stream)                                  \
+    {                                                                                             \
+        return gemm_ptr<U>(ta, tb, m, n, k, alpha, Aa, lda, Ba, ldb, beta, Ca, ldc, batch,        \
+                           (cudaStream_t)stream);                                                 \
+    }                                                                                             \
+    extern "C" int tx_gemm_batched_hostio_##SUF(                                                  \
+        char ta, char tb, int m, int n, int k, const U *alpha, const U *hA, int lda,             \
+        long long lda2, const U *hB, int ldb, long long ldb2, const U *beta, U *hC, int ldc,     \
+        long long ldc2, int batch, tx_stream_t stream, U *dA, U *dB, U *dC)                      \
+    {                                                                                             \
+        return gemm_hostio<U>(ta, tb, m, n, k, alpha, hA, lda, lda2, hB, ldb, ldb2, beta, hC,     \
+                              ldc, ldc2, batch, (cudaStream_t)stream, dA, dB, dC);                \
+    }
+
+TX_STRIDED(s, float)
+TX_STRIDED(d, double)
+TX_STRIDED(c, tx_cfloat)
+TX_STRIDED(z, tx_cdouble)
+
+extern "C" const char *tx_status_string(int status)
+{
+    static const char *args[] = {"ok",    "transa", "transb", "m",     "n",      "k",
+                                 "alpha", "A",      "lda",    "lda2",  "B",      "ldb",
+                                 "ldb2",  "beta",   "C",      "ldc",   "ldc2",   "batch_count",
+                                 "stream", "dA",    "dB",     "dC"};
+    static thread_local char buf[96];
+    if (status == 0) return "success";
+    if (status < 0 && -status < (int)(sizeof(args) / sizeof(args[0]))) {
+        snprintf(buf, sizeof(buf), "invalid argument %d (%s in the strided call)", -status,
+                 args[-status]);
+        return buf;
+    }
+    if (status > 0) return cudaGetErrorString((cudaError_t)status);
+    return "invalid argument";
+}
+
+extern "C" int tx_version(void) { return TX_VERSION; }
+
+extern "C" int tx_last_path(int *launches)
+{
+    if (launches) *launches = t_last_launches;
+    return t_last_path;
+}
+
+extern "C" int tx_set_max_ctas(int v) { return g_max_ctas.exchange(v < 0 ? 0 : v); }
+
+extern "C" int tx_num_instances(void)
+{
+    int c = 0;
+    for (int t = 0; t < 4; ++t) c += tables(t).count;
+    return c;
+}

@@ -1,0 +1,192 @@
+// tx_common.cuh -- scalar types, the paper's entry-wise functors, and the sm_100a
+// PTX wrappers (bulk async copies, mbarriers, cp.async) used by the kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace tx {
+
+// Operation codes for op(X).  For real types 'C' maps to OP_T.
+enum { OP_N = 0, OP_T = 1, OP_C = 2 };
+
+// Path codes reported by tx_last_path() (include/txgemm.h).
+enum { PATH_NONE = 0, PATH_BULK = 1, PATH_GATHER = 2, PATH_PTR = 3, PATH_SCALE = 4,
+       PATH_TAIL = 16 };
+
+template <class T> struct is_cplx { static constexpr bool value = false; };
+template <> struct is_cplx<float2> { static constexpr bool value = true; };
+template <> struct is_cplx<double2> { static constexpr bool value = true; };
+
+// --------------------------------------------------------------------------
+// Entry-wise arithmetic.  acc += op(a) * op(b) with the conjugations folded into
+// the FMA operand signs (compile-time), i.e. the paper's unary_a / unary_b
+// functors (identity / conjugate) applied without extra
+// instructions.  Complex: 4-multiply form.
+// --------------------------------------------------------------------------
+template <bool CA, bool CB>
+__device__ __forceinline__ void mac(float &acc, float a, float b) { acc = fmaf(a, b, acc); }
+template <bool CA, bool CB>
+__device__ __forceinline__ void mac(double &acc, double a, double b) { acc = fma(a, b, acc); }
+template <bool CA, bool CB>
+__device__ __forceinline__ void mac(float2 &acc, float2 a, float2 b)
+{
+    // re += ar*br - (sa*ai)*(sb*bi);  im += ar*(sb*bi) + (sa*ai)*br
+    constexpr float sab = (CA != CB) ? 1.f : -1.f;  // -(sa*sb)
+    constexpr float sb = CB ? -1.f : 1.f, sa = CA ? -1.f : 1.f;
+    acc.x = fmaf(a.x, b.x, acc.x);
+    acc.x = fmaf(sab * a.y, b.y, acc.x);
+    acc.y = fmaf(a.x, sb * b.y, acc.y);
+    acc.y = fmaf(sa * a.y, b.x, acc.y);
+}
+template <bool CA, bool CB>
+__device__ __forceinline__ void mac(double2 &acc, double2 a, double2 b)
+{
+    constexpr double sab = (CA != CB) ? 1.0 : -1.0;
+    constexpr double sb = CB ? -1.0 : 1.0, sa = CA ? -1.0 : 1.0;
+    acc.x = fma(a.x, b.x, acc.x);
+    acc.x = fma(sab * a.y, b.y, acc.x);
+    acc.y = fma(a.x, sb * b.y, acc.y);
+    acc.y = fma(sa * a.y, b.x, acc.y);
+}
+
+template <class T> __host__ __device__ __forceinline__ T zero();
+template <> __host__ __device__ __forceinline__ float zero<float>() { return 0.f; }
+template <> __host__ __device__ __forceinline__ double zero<double>() { return 0.0; }
+template <> __host__ __device__ __forceinline__ float2 zero<float2>() { return make_float2(0.f, 0.f); }
+template <> __host__ __device__ __forceinline__ double2 zero<double2>() { return make_double2(0.0, 0.0); }
+
+// y = a*x (axpby with b == 0: y is never read -- the paper's a1b0 generalised
+// to any alpha) and y = a*x + b*y.
+__device__ __forceinline__ float ax(float a, float x) { return a * x; }
+__device__ __forceinline__ double ax(double a, double x) { return a * x; }
+__device__ __forceinline__ float2 ax(float2 a, float2 x)
+{
+    return make_float2(fmaf(a.x, x.x, -a.y * x.y), fmaf(a.x, x.y, a.y * x.x));
+}
+__device__ __forceinline__ double2 ax(double2 a, double2 x)
+{
+    return make_double2(fma(a.x, x.x, -a.y * x.y), fma(a.x, x.y, a.y * x.x));
+}
+__device__ __forceinline__ float axpby(float a, float x, float b, float y) { return fmaf(b, y, a * x); }
+__device__ __forceinline__ double axpby(double a, double x, double b, double y) { return fma(b, y, a * x); }
+__device__ __forceinline__ float2 axpby(float2 a, float2 x, float2 b, float2 y)
+{
+    float2 r = ax(a, x);
+    r.x = fmaf(b.x, y.x, r.x);
+    r.x = fmaf(-b.y, y.y, r.x);
+    r.y = fmaf(b.x, y.y, r.y);
+    r.y = fmaf(b.y, y.x, r.y);
+    return r;
+}
+__device__ __forceinline__ double2 axpby(double2 a, double2 x, double2 b, double2 y)
+{
+    double2 r = ax(a, x);
+    r.x = fma(b.x, y.x, r.x);
+    r.x = fma(-b.y, y.y, r.x);
+    r.y = fma(b.x, y.y, r.y);
+    r.y = fma(b.y, y.x, r.y);
+    return r;
+}
+
+// --------------------------------------------------------------------------
+// PTX wrappers (sm_90+/sm_100a): mbarrier, 1-D bulk async copies (TMA engine,
+// SASS UBLKCP), async-proxy fence, and element-granular cp.async (LDGSTS).
+// --------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void *p)
+{
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+                 : "memory");
+}
+
+__device__ __forceinline__ void fence_mbar_init()
+{
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity)
+{
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "TX_WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra TX_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+// L2 eviction policy for streamed operands: each byte is used exactly once.
+__device__ __forceinline__ uint64_t policy_evict_first()
+{
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+
+// global -> shared bulk copy, completion counted on an mbarrier (bytes % 16 == 0,
+// both addresses 16-byte aligned).
+__device__ __forceinline__ void bulk_g2s(void *sdst, const void *gsrc, uint32_t bytes,
+                                         uint64_t *bar, uint64_t pol)
+{
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(sdst)),
+        "l"(gsrc), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+        : "memory");
+}
+
+// shared -> global bulk copy, tracked by the issuing thread's bulk groups.
+__device__ __forceinline__ void bulk_s2g(void *gdst, const void *ssrc, uint32_t bytes,
+                                         uint64_t pol)
+{
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(gdst),
+                 "r"(smem_u32(ssrc)), "r"(bytes), "l"(pol)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read()
+{
+    asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait()
+{
+    asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// Make this thread's generic-proxy shared-memory writes visible to the async
+// proxy (required before a bulk store reads them).
+__device__ __forceinline__ void fence_proxy_async_smem()
+{
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// Element-granular async global -> shared copy (LDGSTS), 4/8/16 bytes.
+template <int BYTES>
+__device__ __forceinline__ void cp_async(void *sdst, const void *gsrc)
+{
+    asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(smem_u32(sdst)), "l"(gsrc),
+                 "n"(BYTES)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait()
+{
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+}  // namespace tx

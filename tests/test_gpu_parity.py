@@ -1,0 +1,247 @@
+"""Parity of the CUDA path (through the C ABI) against the CPU oracle.
+
+Element by element on the same seeded inputs: within 1e-5 (s, c) / 1e-13 (d, z)
+normalised by |alpha| sum|op(A)||op(B)| + |beta||C0| (BASELINE.json north_star),
+and bit-exact where the inputs make every order of summation exact.
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_1304_7053_b200 as tx
+import txinputs
+from gpu_util import check, run_lib, run_oracle, to_dev, torch_dtype
+from helpers import NP, OPS_CPLX, OPS_REAL, Operand, random_case, stored_shape
+
+pytestmark = pytest.mark.gpu
+
+
+def ops_for(kind):
+    ops = OPS_CPLX if kind in "cz" else OPS_REAL
+    return [(a, b) for a in ops for b in ops]
+
+
+def _ab(kind, tag, general=True):
+    if not general:
+        return txinputs.scalar(kind, txinputs.stream_key(7, tag, "alpha")), 0
+    return (txinputs.scalar(kind, txinputs.stream_key(7, tag, "alpha")),
+            txinputs.scalar(kind, txinputs.stream_key(7, tag, "beta")))
+
+
+def _case(kind, m, n, k, batch, ta, tb, general, tag, **kw):
+    A, B, C = random_case(kind, m, n, k, batch, ta, tb, seed=101, tag=tag, **kw)
+    alpha, beta = _ab(kind, f"{tag}{kind}{m}{n}{k}{ta}{tb}", general)
+    rc, got, path = run_lib(kind, ta, tb, m, n, k, alpha, beta, A, B, C)
+    assert rc == 0, tx.status_string(rc)
+    ref = run_oracle(kind, ta, tb, m, n, k, alpha, beta, A, B, C)
+    err = check(kind, ta, tb, m, n, k, alpha, beta, A, B, C, got, ref)
+    return err, path, (A, B, C, alpha, beta, got, ref)
+
+
+# ------------------------------------------------------------ the full sweep
+@pytest.mark.parametrize("kind", "sdcz")
+@pytest.mark.parametrize("n", range(1, 17))
+def test_square_sweep_all_ops(kind, n):
+    """Config 3 shape at reduced batch: every op pair, beta == 0 and general,
+    1003 pairs (several tiles and a ragged tail)."""
+    for ta, tb in ops_for(kind):
+        for general in (False, True):
+            err, path, _ = _case(kind, n, n, n, 1003, ta, tb, general, "sweep")
+            assert path[0] in ("bulk", "bulk+tail"), path
+
+
+NONSQUARE = [(8, 16, 4), (16, 3, 16), (1, 16, 16), (16, 16, 1), (5, 7, 3), (16, 1, 7), (2, 9, 13)]
+
+
+@pytest.mark.parametrize("kind", "sdcz")
+@pytest.mark.parametrize("mnk", NONSQUARE, ids=lambda t: "x".join(map(str, t)))
+def test_nonsquare(kind, mnk):
+    m, n, k = mnk
+    for ta, tb in ops_for(kind):
+        for general in (False, True):
+            _case(kind, m, n, k, 517, ta, tb, general, "ns")
+
+
+# ---------------------------------------------------------- exactness / edge
+@pytest.mark.parametrize("kind", "sdcz")
+@pytest.mark.parametrize("n", [1, 3, 4, 8, 13, 16])
+def test_integer_inputs_bit_exact(kind, n):
+    """Integer entries in [-4, 4], integer alpha/beta: every summation order is
+    exact, so GPU == oracle bitwise (compared with ==, +-0 allowed)."""
+    for ta, tb in ops_for(kind):
+        A, B, C = random_case(kind, n, n, n, 777, ta, tb, seed=5, tag="int", dist="int")
+        alpha = txinputs.scalar(kind, 3, dist="int")
+        beta = txinputs.scalar(kind, 4, dist="int")
+        rc, got, _ = run_lib(kind, ta, tb, n, n, n, alpha, beta, A, B, C)
+        assert rc == 0
+        ref = run_oracle(kind, ta, tb, n, n, n, alpha, beta, A, B, C)
+        assert np.array_equal(got, ref), (kind, n, ta, tb)
+
+
+@pytest.mark.parametrize("kind", "sdcz")
+def test_beta0_never_reads_C(kind):
+    for n in (2, 7, 16):
+        A, B, C = random_case(kind, n, n, n, 600, seed=6, tag="nanC", c_sentinel=np.nan)
+        C.buf[:] = np.nan
+        alpha = txinputs.scalar(kind, 9)
+        rc, got, _ = run_lib(kind, "N", "N", n, n, n, alpha, 0, A, B, C)
+        assert rc == 0
+        assert np.all(np.isfinite(C.dense(got)))
+        ref = run_oracle(kind, "N", "N", n, n, n, alpha, 0, A, B, C)
+        check(kind, "N", "N", n, n, n, alpha, 0, A, B, C, got, ref)
+
+
+@pytest.mark.parametrize("kind", "sdcz")
+def test_alpha0_and_k0_scale_C(kind):
+    for alpha, k in ((0, 5), (1.5, 0)):
+        A, B, C = random_case(kind, 5, 6, max(k, 1), 300, seed=7, tag="a0", dist="int")
+        A.buf[:] = np.nan
+        B.buf[:] = np.nan
+        beta = txinputs.scalar(kind, 5, dist="int")
+        rc, got, path = run_lib(kind, "N", "N", 5, 6, k, alpha, beta, A, B, C)
+        assert rc == 0 and path[0] == "scale"
+        ref = run_oracle(kind, "N", "N", 5, 6, k, alpha, beta, A, B, C)
+        assert np.array_equal(got, ref)
+        # beta == 0: C <- 0 without reading C
+        C.buf[:] = np.nan
+        rc, got, _ = run_lib(kind, "N", "N", 5, 6, k, alpha, 0, A, B, C)
+        assert rc == 0 and np.all(C.dense(got) == 0)
+
+
+@pytest.mark.parametrize("kind", "sdcz")
+def test_padded_layout_and_sentinels(kind):
+    """General strided path (ld > rows, ld2 > ld*cols): same values as the oracle,
+    pad entries of C bitwise untouched."""
+    for n, ta, tb in ((5, "N", "T"), (16, "T", "N"), (9, "C", "C")):
+        if kind in "sd":
+            ta, tb = ta.replace("C", "T"), tb.replace("C", "T")
+        A, B, C = random_case(kind, n, n, n, 333, ta, tb, seed=8, tag="pad", pad=(3, 5),
+                              c_sentinel=-3.75)
+        alpha, beta = _ab(kind, "pad")
+        rc, got, path = run_lib(kind, ta, tb, n, n, n, alpha, beta, A, B, C)
+        assert rc == 0 and path[0] == "gather", path
+        ref = run_oracle(kind, ta, tb, n, n, n, alpha, beta, A, B, C)
+        check(kind, ta, tb, n, n, n, alpha, beta, A, B, C, got, ref)
+        mask = C.mask()
+        assert np.array_equal(got[~mask].view(np.uint8), C.buf[~mask].view(np.uint8))
+
+
+@pytest.mark.parametrize("kind", "sdcz")
+def test_misaligned_base_uses_gather(kind):
+    A, B, C = random_case(kind, 8, 8, 8, 257, seed=9, tag="mis")
+    alpha, beta = _ab(kind, "mis")
+    rc, got, path = run_lib(kind, "N", "N", 8, 8, 8, alpha, beta, A, B, C, misalign=1)
+    assert rc == 0
+    if kind != "z":
+        assert path[0] == "gather"
+    ref = run_oracle(kind, "N", "N", 8, 8, 8, alpha, beta, A, B, C)
+    check(kind, "N", "N", 8, 8, 8, alpha, beta, A, B, C, got, ref)
+
+
+@pytest.mark.parametrize("kind", "sdcz")
+def test_broadcast_A_ld2_zero(kind):
+    """lda2 = 0: one A for every pair (the paper's fixed-operand variant, §9)."""
+    n, batch = 6, 411
+    A, B, C = random_case(kind, n, n, n, batch, seed=10, tag="bc")
+    A1 = Operand(kind, n, n, 1, txinputs.stream_key(10, "bcA"))
+    A1.ld2 = 0
+    A1.batch = batch
+    alpha, beta = _ab(kind, "bc")
+    rc, got, _ = run_lib(kind, "N", "N", n, n, n, alpha, beta, A1, B, C)
+    assert rc == 0
+    ref = run_oracle(kind, "N", "N", n, n, n, alpha, beta, A1, B, C)
+    check(kind, "N", "N", n, n, n, alpha, beta, A1, B, C, got, ref)
+
+
+@pytest.mark.parametrize("kind", "sdcz")
+@pytest.mark.parametrize("batch", [1, 2, 3, 15, 17, 4099])
+def test_batch_edges(kind, batch):
+    for n in (1, 3, 16):
+        _case(kind, n, n, n, batch, "N", "N", True, f"be{batch}")
+
+
+# ------------------------------------------------------ pointer-array layout
+@pytest.mark.parametrize("kind", "sdcz")
+def test_pointer_array_equals_strided_and_oracle(kind):
+    import torch
+
+    for (m, n, k) in ((8, 16, 4), (16, 3, 16), (7, 7, 7)):
+        for ta, tb in ops_for(kind)[::2]:
+            A, B, C = random_case(kind, m, n, k, 999, ta, tb, seed=11, tag="ptr")
+            alpha, beta = _ab(kind, "ptr")
+            rc, got_strided, _ = run_lib(kind, ta, tb, m, n, k, alpha, beta, A, B, C)
+            assert rc == 0
+            perm = np.random.default_rng(2).permutation(C.batch)
+            dA, _ = to_dev(A)
+            dB, _ = to_dev(B)
+            dC, _ = to_dev(C)
+            es = dA.element_size()
+            pa = torch.tensor(A.offsets()[perm] * es + dA.data_ptr(), device="cuda")
+            pb = torch.tensor(B.offsets()[perm] * es + dB.data_ptr(), device="cuda")
+            pc = torch.tensor(C.offsets()[perm] * es + dC.data_ptr(), device="cuda")
+            rc = tx.tx_gemm_batched_ptr(kind, ta, tb, m, n, k, alpha, pa, A.ld, pb, B.ld, beta, pc,
+                                        C.ld, C.batch)
+            assert rc == 0 and tx.last_path()[0] == "ptr"
+            got = dC.cpu().numpy()
+            # each pair is independent: permuting the pointers permutes nothing in the result
+            assert np.array_equal(got.view(np.uint8), got_strided.view(np.uint8))
+            ref = run_oracle(kind, ta, tb, m, n, k, alpha, beta, A, B, C)
+            check(kind, ta, tb, m, n, k, alpha, beta, A, B, C, got, ref)
+
+
+# ------------------------------------------------------------- determinism
+@pytest.mark.parametrize("kind", "sz")
+def test_deterministic_across_grid_sizes(kind):
+    n = 16
+    A, B, C = random_case(kind, n, n, n, 5000, seed=12, tag="det")
+    alpha, beta = _ab(kind, "det")
+    outs = []
+    for cap in (0, 1, 7, 148):
+        prev = tx.set_max_ctas(cap)
+        try:
+            rc, got, _ = run_lib(kind, "N", "T", n, n, n, alpha, beta, A, B, C)
+        finally:
+            tx.set_max_ctas(prev)
+        assert rc == 0
+        outs.append(got)
+    for o in outs[1:]:
+        assert np.array_equal(o.view(np.uint8), outs[0].view(np.uint8))
+
+
+# ----------------------------------------------------------- host-buffer API
+@pytest.mark.parametrize("kind", "sdcz")
+def test_hostio_equals_device_path(kind):
+    import torch
+
+    n, batch = 10, 2000
+    A, B, C = random_case(kind, n, n, n, batch, seed=13, tag="hio")
+    alpha, beta = _ab(kind, "hio")
+    rc, got_dev, _ = run_lib(kind, "N", "N", n, n, n, alpha, beta, A, B, C)
+    hA = torch.from_numpy(A.buf.copy()).pin_memory()
+    hB = torch.from_numpy(B.buf.copy()).pin_memory()
+    hC = torch.from_numpy(C.buf.copy()).pin_memory()
+    dA, dB, dC = (torch.empty_like(x, device="cuda") for x in (hA, hB, hC))
+    rc = tx.tx_gemm_batched_hostio(kind, "N", "N", n, n, n, alpha, hA.data_ptr(), A.ld, A.ld2,
+                                   hB.data_ptr(), B.ld, B.ld2, beta, hC.data_ptr(), C.ld, C.ld2,
+                                   batch, torch.cuda.current_stream(), dA, dB, dC)
+    assert rc == 0
+    torch.cuda.synchronize()
+    assert np.array_equal(hC.numpy().view(np.uint8), got_dev.view(np.uint8))
+
+
+# ------------------------------------------------- tensor API
+def test_tensor_api_matches_torch_layout():
+    import torch
+
+    kind, m, n, k, batch = "d", 5, 6, 7, 300
+    A, B, C = random_case(kind, m, n, k, batch, seed=14, tag="tapi")
+    At = torch.from_numpy(A.buf.copy()).cuda().view(batch, k, m).transpose(1, 2)
+    Bt = torch.from_numpy(B.buf.copy()).cuda().view(batch, n, k).transpose(1, 2)
+    Ct = torch.from_numpy(C.buf.copy()).cuda().view(batch, n, m).transpose(1, 2)
+    tx.gemm_batched(At, Bt, Ct, "N", "N", 0.5, 0.25)
+    torch.cuda.synchronize()
+    ref = run_oracle(kind, "N", "N", m, n, k, 0.5, 0.25, A, B, C)
+    got = Ct.transpose(1, 2).contiguous().view(-1).cpu().numpy()
+    check(kind, "N", "N", m, n, k, 0.5, 0.25, A, B, C, got, ref)
