@@ -14,8 +14,8 @@
 //    layout: minimal leading dimensions).  Each tile of each
 //    operand is ONE contiguous run of bytes, so a single thread moves it with a
 //    1-D bulk async copy (TMA engine, cp.async.bulk) into an S-stage ring tracked
-//    by mbarriers, and C goes back with a bulk store from a double-buffered
-//    output tile.  Persistent CTAs loop over tiles (the paper's "each CUDA
+//    by mbarriers; C is stored from registers with coalesced vector stores.
+//    Persistent CTAs loop over tiles (the paper's "each CUDA
 //    thread-block is used to process multiple matrices").
 //  * gather_kernel -- any strided layout (padded ld/ld2, broadcast ld2 = 0,
 //    unaligned bases) and the pointer-array layout: element-
@@ -46,38 +46,108 @@ struct Params {
 };
 
 // --------------------------------------------------------------------------
-// Register micro-tile: rows i0..i0+RM-1, cols j0..j0+RN-1 of one C^p.
-//   a: stored A^p in shared memory, packed (ld = rows of stored A)
-//   b: stored B^p in shared memory, packed
-//   cin: packed input C^p (beta != 0), cout/ldo: output location.
-// MS/NS/KS are the compile-time sizes (0 = use m/n/k).
+// Thread mapping (chosen per instance by tools/mapsearch.cpp, see
+// tx_map_table.inc): each thread owns an RM x RN micro-tile of one C^p.
+//   rows  i_r = rb*RM + r (RMODE 0) | rb + RB*r (RMODE 1)
+//   cols  j_c = cb*RN + c (CMODE 0) | cb + CB*c (CMODE 1), then rotated by
+//         q*ROTN (mod n) so neighbouring matrices hit different banks
+//   lanes rb fastest (LO 0) | cb fastest (LO 1)
+//   VA/VB/VC: vector width (elements) of the shared-memory accesses of A, B
+//         and C along their stored-contiguous dimension.
+// Every mapping accumulates each output over l = 0..k-1 in ascending order, so
+// all mappings (and the gather / pointer paths) give bitwise-identical results.
 // --------------------------------------------------------------------------
-template <class T, int MS, int NS, int KS, int OPA, int OPB, bool B0, int RM, int RN>
+template <int RM_, int RN_, int RMODE_, int CMODE_, int LO_, int VA_, int VB_, int VC_, int ROTN_>
+struct MapT {
+    static constexpr int RM = RM_, RN = RN_, RMODE = RMODE_, CMODE = CMODE_, LO = LO_;
+    static constexpr int VA = VA_, VB = VB_, VC = VC_, ROTN = ROTN_;
+};
+
+template <class T, int V>
+__device__ __forceinline__ void ldv(const T *p, T *out)
+{
+    if constexpr (V == 1) {
+        out[0] = *p;
+    } else if constexpr (V * sizeof(T) == 16) {
+        const float4 u = *reinterpret_cast<const float4 *>(p);
+        memcpy(out, &u, 16);
+    } else {
+        static_assert(V * sizeof(T) == 8, "vector width");
+        const float2 u = *reinterpret_cast<const float2 *>(p);
+        memcpy(out, &u, 8);
+    }
+}
+template <class T, int V>
+__device__ __forceinline__ void stv(T *p, const T *in)
+{
+    if constexpr (V == 1) {
+        *p = in[0];
+    } else if constexpr (V * sizeof(T) == 16) {
+        float4 u;
+        memcpy(&u, in, 16);
+        *reinterpret_cast<float4 *>(p) = u;
+    } else {
+        float2 u;
+        memcpy(&u, in, 8);
+        *reinterpret_cast<float2 *>(p) = u;
+    }
+}
+
+// One micro-tile of one C^p.
+//   a, b: stored A^p, B^p in shared memory, packed (ld = stored rows)
+//   cin : packed input C^p in shared memory (beta != 0)
+//   cout/ldo: destination of C^p (global memory, true leading dimension)
+// MS/NS/KS are compile-time sizes (0 = use m_/n_/k_; then the mapping must be
+// scalar, VA = VB = VC = 1).
+template <class T, int MS, int NS, int KS, int OPA, int OPB, bool B0, class MP>
 __device__ __forceinline__ void micro_tile(const T *__restrict__ a, const T *__restrict__ b,
                                            const T *__restrict__ cin, T *__restrict__ cout,
-                                           int ldo, int i0, int j0, int m_, int n_, int k_,
-                                           T alpha, T beta)
+                                           long long ldo, int rb, int cb, int q, int m_, int n_,
+                                           int k_, T alpha, T beta)
 {
+    constexpr int RM = MP::RM, RN = MP::RN;
     constexpr bool CA = (OPA == OP_C), CBc = (OPB == OP_C);
+    constexpr int VA = MP::VA, VB = MP::VB, VC = MP::VC;
+    constexpr int VLa = (OPA != OP_N && VA > 1) ? VA : 1;   // A vectors run along l
+    constexpr int VLb = (OPB == OP_N && VB > 1) ? VB : 1;   // B vectors run along l
+    constexpr int VL = VLa > VLb ? VLa : VLb;
     constexpr int KMAX = KS ? KS : 16;
     const int m = MS ? MS : m_;
     const int n = NS ? NS : n_;
     const int k = KS ? KS : k_;
-    // op(A)_{il} = a[i + m*l] (N) or a[l + k*i] (T/C); op(B)_{lj} = b[l + k*j] (N) or b[j + n*l].
-    const int sa = (OPA == OP_N) ? m : 1;
-    const int sb = (OPB == OP_N) ? 1 : n;
-    const T *ar[RM];
-    const T *bc[RN];
+    const int RB = (m + RM - 1) / RM, CB = (n + RN - 1) / RN;
+
+    // ---- rows and columns owned by this thread
+    int ir[RM];
+    bool rv[RM];
 #pragma unroll
     for (int r = 0; r < RM; ++r) {
-        const int i = min(i0 + r, m - 1);  // clamp: rows >= m are computed but never stored
-        ar[r] = (OPA == OP_N) ? a + i : a + i * k;
+        const int i = MP::RMODE == 0 ? rb * RM + r : rb + RB * r;
+        rv[r] = i < m;
+        ir[r] = min(i, m - 1);  // rows >= m are computed but never stored
     }
+    if constexpr (MP::RMODE == 0 && (VA > 1 || VC > 1)) {
+        // vector groups start on a multiple of the vector width (m % V == 0)
+        constexpr int V = VA > VC ? VA : VC;
+#pragma unroll
+        for (int g = 0; g < RM; g += V) {
+            const int i0 = min(rb * RM + g, m - V);
+#pragma unroll
+            for (int t = 0; t < V; ++t) ir[g + t] = i0 + t;
+        }
+    }
+    int jc[RN];
+    bool cv[RN];
 #pragma unroll
     for (int c = 0; c < RN; ++c) {
-        const int j = min(j0 + c, n - 1);
-        bc[c] = (OPB == OP_N) ? b + j * k : b + j;
+        int j = MP::CMODE == 0 ? cb * RN + c : cb + CB * c;
+        cv[c] = j < n;
+        j = min(j, n - 1);
+        if constexpr (OPB != OP_N && VB > 1) j = min(cb * RN + (c / VB) * VB, n - VB) + c % VB;
+        if constexpr (MP::ROTN != 0) j = (j + q * MP::ROTN) % n;
+        jc[c] = j;
     }
+
     T acc[RM][RN];
 #pragma unroll
     for (int r = 0; r < RM; ++r)
@@ -85,58 +155,85 @@ __device__ __forceinline__ void micro_tile(const T *__restrict__ a, const T *__r
         for (int c = 0; c < RN; ++c) acc[r][c] = zero<T>();
 
 #pragma unroll
-    for (int l = 0; l < KMAX; ++l) {
-        if (KS == 0 && l >= k) break;
-        T av[RM], bv[RN];
+    for (int l0 = 0; l0 < KMAX; l0 += VL) {
+        if (KS == 0 && l0 >= k) break;
+        T av[RM][VL], bv[RN][VL];
+        // op(A)_{il}: a[i + m*l] (N) or a[l + k*i] (T/C)
+        if constexpr (OPA == OP_N) {
 #pragma unroll
-        for (int r = 0; r < RM; ++r) av[r] = ar[r][l * sa];
+            for (int g = 0; g < RM; g += VA)
 #pragma unroll
-        for (int c = 0; c < RN; ++c) bv[c] = bc[c][l * sb];
+                for (int t = 0; t < VL; ++t) {
+                    T tmp[VA];
+                    ldv<T, VA>(a + ir[g] + m * (l0 + t), tmp);
 #pragma unroll
-        for (int r = 0; r < RM; ++r)
+                    for (int e = 0; e < VA; ++e) av[g + e][t] = tmp[e];
+                }
+        } else {
 #pragma unroll
-            for (int c = 0; c < RN; ++c) mac<CA, CBc>(acc[r][c], av[r], bv[c]);
+            for (int r = 0; r < RM; ++r)
+#pragma unroll
+                for (int t = 0; t < VL; t += VLa) ldv<T, VLa>(a + (l0 + t) + k * ir[r], &av[r][t]);
+        }
+        // op(B)_{lj}: b[l + k*j] (N) or b[j + n*l] (T/C)
+        if constexpr (OPB == OP_N) {
+#pragma unroll
+            for (int c = 0; c < RN; ++c)
+#pragma unroll
+                for (int t = 0; t < VL; t += VLb) ldv<T, VLb>(b + (l0 + t) + k * jc[c], &bv[c][t]);
+        } else {
+#pragma unroll
+            for (int g = 0; g < RN; g += VB)
+#pragma unroll
+                for (int t = 0; t < VL; ++t) {
+                    T tmp[VB];
+                    ldv<T, VB>(b + jc[g] + n * (l0 + t), tmp);
+#pragma unroll
+                    for (int e = 0; e < VB; ++e) bv[g + e][t] = tmp[e];
+                }
+        }
+#pragma unroll
+        for (int t = 0; t < VL; ++t)
+#pragma unroll
+            for (int r = 0; r < RM; ++r)
+#pragma unroll
+                for (int c = 0; c < RN; ++c) mac<CA, CBc>(acc[r][c], av[r][t], bv[c][t]);
     }
 
-    constexpr bool FULLM = MS && (MS % RM == 0);
-    constexpr bool FULLN = NS && (NS % RN == 0);
+    // ---- epilogue (the paper's axpby functors)
 #pragma unroll
     for (int c = 0; c < RN; ++c) {
-        const int j = j0 + c;
-        if (!FULLN && j >= n) continue;
+        if (!cv[c]) continue;
+        const int j = jc[c];
 #pragma unroll
-        for (int r = 0; r < RM; ++r) {
-            const int i = i0 + r;
-            if (!FULLM && i >= m) continue;
-            T y;
-            if constexpr (B0)
-                y = ax(alpha, acc[r][c]);
-            else
-                y = axpby(alpha, acc[r][c], beta, cin[i + m * j]);
-            cout[i + (long long)ldo * j] = y;
+        for (int g = 0; g < RM; g += VC) {
+            if (!rv[g]) continue;
+            const int i = ir[g];
+            T y[VC];
+            if constexpr (B0) {
+#pragma unroll
+                for (int e = 0; e < VC; ++e) y[e] = ax(alpha, acc[g + e][c]);
+            } else {
+                T x[VC];
+                ldv<T, VC>(cin + i + m * j, x);
+#pragma unroll
+                for (int e = 0; e < VC; ++e) y[e] = axpby(alpha, acc[g + e][c], beta, x[e]);
+            }
+            stv<T, VC>(cout + i + ldo * j, y);
         }
     }
 }
 
 // Threads -> (matrix q of the tile, row block, column block) work items.
-template <class T, int MS, int NS, int KS, int OPA, int OPB, bool B0, int RM, int RN, int NT>
-__device__ __forceinline__ void compute_tile_to_smem(const T *sA, const T *sB, const T *sC,
-                                                     T *out, int np, const Params<T> &p)
+template <class MP>
+__device__ __forceinline__ void split_item(int sub, int RB, int CB, int &rb, int &cb)
 {
-    const int m = MS ? MS : p.m, n = NS ? NS : p.n, k = KS ? KS : p.k;
-    const int SA = m * k, SB = k * n, SC = m * n;
-    const int CBn = (n + RN - 1) / RN;
-    const int TPM = ((m + RM - 1) / RM) * CBn;
-    const int items = np * TPM;
-    for (int w = threadIdx.x; w < items; w += NT) {
-        const int q = w / TPM;
-        const int sub = w - q * TPM;
-        const int rb = sub / CBn;
-        const int cb = sub - rb * CBn;
-        micro_tile<T, MS, NS, KS, OPA, OPB, B0, RM, RN>(sA + q * SA, sB + q * SB,
-                                                         B0 ? nullptr : sC + q * SC, out + q * SC,
-                                                         m, rb * RM, cb * RN, m, n, k, p.alpha,
-                                                         p.beta);
+    if constexpr (MP::LO == 0) {
+        rb = sub % RB;
+        cb = sub / RB;
+    } else {
+        cb = sub % CB;
+        rb = sub / CB;
     }
 }
 
@@ -145,20 +242,22 @@ __device__ __forceinline__ void compute_tile_to_smem(const T *sA, const T *sB, c
 // Preconditions (host-checked): lda = rows(A), lda2 = rows(A)*cols(A) (same for
 // B, C), base pointers 16-byte aligned, batch and P multiples of the 16-byte
 // alignment unit, k >= 1, alpha != 0.
-// Shared memory: S stages of [A tile | B tile | C-in tile], 2 output tiles,
-// S mbarriers.
+// Shared memory: S stages of [A tile | B tile | C-in tile] and S mbarriers.
+// C^p is stored from registers straight to global memory (vectorised along the
+// contiguous rows by the mapping), so no output staging is needed.
 // --------------------------------------------------------------------------
-template <class T, int MS, int NS, int KS, int OPA, int OPB, bool B0, int RM, int RN, int NT>
+template <class T, int MS, int NS, int KS, int OPA, int OPB, bool B0, class MP, int NT>
 __global__ void __launch_bounds__(NT) bulk_kernel(const Params<T> p)
 {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int m = MS ? MS : p.m, n = NS ? NS : p.n, k = KS ? KS : p.k;
     const int SA = m * k, SB = k * n, SC = m * n;
+    const int RB = (m + MP::RM - 1) / MP::RM, CB = (n + MP::RN - 1) / MP::RN;
+    const int TPM = RB * CB;
     const int P = p.P, S = p.S;
     const int stage_elems = P * (SA + SB + (B0 ? 0 : SC));
     T *stage0 = reinterpret_cast<T *>(smem_raw);
-    T *out0 = stage0 + (long long)S * stage_elems;
-    uint64_t *bars = reinterpret_cast<uint64_t *>(out0 + 2 * P * SC);
+    uint64_t *bars = reinterpret_cast<uint64_t *>(stage0 + (long long)S * stage_elems);
 
     const int tid = threadIdx.x;
     const int G = gridDim.x;
@@ -172,8 +271,7 @@ __global__ void __launch_bounds__(NT) bulk_kernel(const Params<T> p)
     __syncthreads();
 
     auto issue = [&](int i) {  // local tile i -> stage i % S (thread 0 only)
-        const long long t = blockIdx.x + (long long)i * G;
-        const long long pair0 = t * P;
+        const long long pair0 = (blockIdx.x + (long long)i * G) * P;
         const int np = (int)min((long long)P, p.batch - pair0);
         T *st = stage0 + (long long)(i % S) * stage_elems;
         const uint32_t ba = np * SA * (uint32_t)sizeof(T);
@@ -193,21 +291,21 @@ __global__ void __launch_bounds__(NT) bulk_kernel(const Params<T> p)
         if (tid == 0 && i + S - 1 < my_tiles) issue(i + S - 1);
         const long long pair0 = (blockIdx.x + (long long)i * G) * P;
         const int np = (int)min((long long)P, p.batch - pair0);
-        T *st = stage0 + (long long)(i % S) * stage_elems;
-        T *out = out0 + (i & 1) * P * SC;
+        const T *st = stage0 + (long long)(i % S) * stage_elems;
+        const T *sA = st, *sB = st + P * SA, *sC = st + P * (SA + SB);
+        T *gC = p.C + pair0 * SC;
         mbar_wait(&bars[i % S], (i / S) & 1);
-        compute_tile_to_smem<T, MS, NS, KS, OPA, OPB, B0, RM, RN, NT>(st, st + P * SA,
-                                                                       st + P * (SA + SB), out,
-                                                                       np, p);
-        fence_proxy_async_smem();      // our st.shared -> visible to the bulk store
-        if (tid == 0) bulk_wait_read<0>();  // store of tile i-1 has finished reading out[(i+1)&1]
-        __syncthreads();               // tile i consumed (stage free), out[i&1] complete
-        if (tid == 0) {
-            bulk_s2g(p.C + pair0 * SC, out, np * SC * (uint32_t)sizeof(T), pol);
-            bulk_commit();
+        const int items = np * TPM;
+        for (int w = tid; w < items; w += NT) {
+            const int q = w / TPM;
+            int rb, cb;
+            split_item<MP>(w - q * TPM, RB, CB, rb, cb);
+            micro_tile<T, MS, NS, KS, OPA, OPB, B0, MP>(sA + q * SA, sB + q * SB,
+                                                        B0 ? nullptr : sC + q * SC, gC + q * SC,
+                                                        m, rb, cb, q, m, n, k, p.alpha, p.beta);
         }
+        __syncthreads();  // stage i % S fully consumed before it is refilled
     }
-    if (tid == 0) bulk_wait<0>();
 }
 
 // --------------------------------------------------------------------------
@@ -217,7 +315,7 @@ __global__ void __launch_bounds__(NT) bulk_kernel(const Params<T> p)
 // --------------------------------------------------------------------------
 constexpr int GS = 3;
 
-template <class T, int OPA, int OPB, bool B0, int RM, int RN, int NT, bool PTR>
+template <class T, int OPA, int OPB, bool B0, class MP, int NT, bool PTR>
 __global__ void __launch_bounds__(NT) gather_kernel(const Params<T> p)
 {
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -264,8 +362,8 @@ __global__ void __launch_bounds__(NT) gather_kernel(const Params<T> p)
         if (i < my_tiles) issue(i);
         cp_async_commit();
     }
-    const int CBn = (n + RN - 1) / RN;
-    const int TPM = ((m + RM - 1) / RM) * CBn;
+    const int RB = (m + MP::RM - 1) / MP::RM, CB = (n + MP::RN - 1) / MP::RN;
+    const int TPM = RB * CB;
     for (int i = 0; i < my_tiles; ++i) {
         if (i + GS - 1 < my_tiles) issue(i + GS - 1);
         cp_async_commit();
@@ -278,13 +376,12 @@ __global__ void __launch_bounds__(NT) gather_kernel(const Params<T> p)
         const int items = np * TPM;
         for (int w = tid; w < items; w += NT) {
             const int q = w / TPM;
-            const int sub = w - q * TPM;
-            const int rb = sub / CBn, cb = sub - rb * CBn;
+            int rb, cb;
+            split_item<MP>(w - q * TPM, RB, CB, rb, cb);
             T *cout = PTR ? p.Cp[pair0 + q] : p.C + (pair0 + q) * p.ldc2;
-            micro_tile<T, 0, 0, 0, OPA, OPB, B0, RM, RN>(sA + q * SA, sB + q * SB,
-                                                         B0 ? nullptr : sC + q * SC, cout, p.ldc,
-                                                         rb * RM, cb * RN, m, n, k, p.alpha,
-                                                         p.beta);
+            micro_tile<T, 0, 0, 0, OPA, OPB, B0, MP>(sA + q * SA, sB + q * SB,
+                                                     B0 ? nullptr : sC + q * SC, cout, p.ldc, rb,
+                                                     cb, q, m, n, k, p.alpha, p.beta);
         }
         __syncthreads();
     }
