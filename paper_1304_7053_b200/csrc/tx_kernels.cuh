@@ -126,9 +126,11 @@ __device__ __forceinline__ void micro_tile(const T *__restrict__ a, const T *__r
         rv[r] = i < m;
         ir[r] = min(i, m - 1);  // rows >= m are computed but never stored
     }
-    if constexpr (MP::RMODE == 0 && (VA > 1 || VC > 1)) {
+    constexpr int VAr = (OPA == OP_N) ? VA : 1;  // A vectors that run along the rows
+    if constexpr (MP::RMODE == 0 && (VAr > 1 || VC > 1)) {
         // vector groups start on a multiple of the vector width (m % V == 0)
-        constexpr int V = VA > VC ? VA : VC;
+        constexpr int V = VAr > VC ? VAr : VC;
+        static_assert(RM % V == 0, "row vector groups");
 #pragma unroll
         for (int g = 0; g < RM; g += V) {
             const int i0 = min(rb * RM + g, m - V);
@@ -143,7 +145,10 @@ __device__ __forceinline__ void micro_tile(const T *__restrict__ a, const T *__r
         int j = MP::CMODE == 0 ? cb * RN + c : cb + CB * c;
         cv[c] = j < n;
         j = min(j, n - 1);
-        if constexpr (OPB != OP_N && VB > 1) j = min(cb * RN + (c / VB) * VB, n - VB) + c % VB;
+        if constexpr (OPB != OP_N && VB > 1) {
+            static_assert(MP::CMODE == 0 && RN % VB == 0, "column vector groups");
+            j = min(cb * RN + (c / VB) * VB, n - VB) + c % VB;
+        }
         if constexpr (MP::ROTN != 0) j = (j + q * MP::ROTN) % n;
         jc[c] = j;
     }
