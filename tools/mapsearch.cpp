@@ -234,10 +234,11 @@ int main(int argc, char **argv)
                             if (rms.empty() || rms.back() != r) rms.push_back(r);
                         }
                         rns = rms;
-                        // occupancy floor: 8 computing warps per SM need 256/tpm pairs in the
-                        // computing stages plus ~1.5x that in flight within ~220 KB of smem
+                        // occupancy floor: a 128-thread CTA computes on 128/tpm pairs per
+                        // stage; 2 CTAs per SM with 4 stages each must fit in ~110 KB, so a
+                        // stage holds at most 27 KB: tpm >= 128 * in_bytes / 27 KB.
                         const int in_bytes = (n * n * 2 + (b0 ? 0 : n * n)) * t.es;
-                        int tpm_min = (int)((long)in_bytes * 640 / 225280) + 1;
+                        int tpm_min = (int)((128L * in_bytes + 27647) / 27648);
                         if (tpm_min > n * n) tpm_min = n * n;
                         for (int RM : rms)
                             for (int RN : rns) {
