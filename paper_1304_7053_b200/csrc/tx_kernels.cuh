@@ -23,6 +23,8 @@
 //    written straight from registers.
 #pragma once
 
+#include <type_traits>
+
 #include "tx_common.cuh"
 
 namespace tx {
@@ -63,33 +65,53 @@ struct MapT {
     static constexpr int VA = VA_, VB = VB_, VC = VC_, ROTN = ROTN_;
 };
 
+// Vector shared/global accesses of V consecutive elements, moved element by
+// element through registers (no memcpy through pointers into local arrays,
+// which made ptxas spill to local memory).
 template <class T, int V>
-__device__ __forceinline__ void ldv(const T *p, T *out)
+struct Vec {
+    T v[V];
+};
+
+template <class T, int V>
+__device__ __forceinline__ Vec<T, V> ldv(const T *p)
 {
+    Vec<T, V> r;
     if constexpr (V == 1) {
-        out[0] = *p;
-    } else if constexpr (V * sizeof(T) == 16) {
+        r.v[0] = *p;
+    } else if constexpr (std::is_same<T, float>::value && V == 4) {
         const float4 u = *reinterpret_cast<const float4 *>(p);
-        memcpy(out, &u, 16);
-    } else {
-        static_assert(V * sizeof(T) == 8, "vector width");
+        r.v[0] = u.x; r.v[1] = u.y; r.v[2] = u.z; r.v[3] = u.w;
+    } else if constexpr (std::is_same<T, float>::value && V == 2) {
         const float2 u = *reinterpret_cast<const float2 *>(p);
-        memcpy(out, &u, 8);
+        r.v[0] = u.x; r.v[1] = u.y;
+    } else if constexpr (std::is_same<T, double>::value && V == 2) {
+        const double2 u = *reinterpret_cast<const double2 *>(p);
+        r.v[0] = u.x; r.v[1] = u.y;
+    } else if constexpr (std::is_same<T, float2>::value && V == 2) {
+        const float4 u = *reinterpret_cast<const float4 *>(p);
+        r.v[0] = make_float2(u.x, u.y); r.v[1] = make_float2(u.z, u.w);
+    } else {
+        static_assert(V == 1, "unsupported vector width");
     }
+    return r;
 }
+
 template <class T, int V>
-__device__ __forceinline__ void stv(T *p, const T *in)
+__device__ __forceinline__ void stv(T *p, const Vec<T, V> &r)
 {
     if constexpr (V == 1) {
-        *p = in[0];
-    } else if constexpr (V * sizeof(T) == 16) {
-        float4 u;
-        memcpy(&u, in, 16);
-        *reinterpret_cast<float4 *>(p) = u;
+        *p = r.v[0];
+    } else if constexpr (std::is_same<T, float>::value && V == 4) {
+        *reinterpret_cast<float4 *>(p) = make_float4(r.v[0], r.v[1], r.v[2], r.v[3]);
+    } else if constexpr (std::is_same<T, float>::value && V == 2) {
+        *reinterpret_cast<float2 *>(p) = make_float2(r.v[0], r.v[1]);
+    } else if constexpr (std::is_same<T, double>::value && V == 2) {
+        *reinterpret_cast<double2 *>(p) = make_double2(r.v[0], r.v[1]);
+    } else if constexpr (std::is_same<T, float2>::value && V == 2) {
+        *reinterpret_cast<float4 *>(p) = make_float4(r.v[0].x, r.v[0].y, r.v[1].x, r.v[1].y);
     } else {
-        float2 u;
-        memcpy(&u, in, 8);
-        *reinterpret_cast<float2 *>(p) = u;
+        static_assert(V == 1, "unsupported vector width");
     }
 }
 
@@ -169,32 +191,38 @@ __device__ __forceinline__ void micro_tile(const T *__restrict__ a, const T *__r
             for (int g = 0; g < RM; g += VA)
 #pragma unroll
                 for (int t = 0; t < VL; ++t) {
-                    T tmp[VA];
-                    ldv<T, VA>(a + ir[g] + m * (l0 + t), tmp);
+                    const Vec<T, VA> u = ldv<T, VA>(a + ir[g] + m * (l0 + t));
 #pragma unroll
-                    for (int e = 0; e < VA; ++e) av[g + e][t] = tmp[e];
+                    for (int e = 0; e < VA; ++e) av[g + e][t] = u.v[e];
                 }
         } else {
 #pragma unroll
             for (int r = 0; r < RM; ++r)
 #pragma unroll
-                for (int t = 0; t < VL; t += VLa) ldv<T, VLa>(a + (l0 + t) + k * ir[r], &av[r][t]);
+                for (int t = 0; t < VL; t += VLa) {
+                    const Vec<T, VLa> u = ldv<T, VLa>(a + (l0 + t) + k * ir[r]);
+#pragma unroll
+                    for (int e = 0; e < VLa; ++e) av[r][t + e] = u.v[e];
+                }
         }
         // op(B)_{lj}: b[l + k*j] (N) or b[j + n*l] (T/C)
         if constexpr (OPB == OP_N) {
 #pragma unroll
             for (int c = 0; c < RN; ++c)
 #pragma unroll
-                for (int t = 0; t < VL; t += VLb) ldv<T, VLb>(b + (l0 + t) + k * jc[c], &bv[c][t]);
+                for (int t = 0; t < VL; t += VLb) {
+                    const Vec<T, VLb> u = ldv<T, VLb>(b + (l0 + t) + k * jc[c]);
+#pragma unroll
+                    for (int e = 0; e < VLb; ++e) bv[c][t + e] = u.v[e];
+                }
         } else {
 #pragma unroll
             for (int g = 0; g < RN; g += VB)
 #pragma unroll
                 for (int t = 0; t < VL; ++t) {
-                    T tmp[VB];
-                    ldv<T, VB>(b + jc[g] + n * (l0 + t), tmp);
+                    const Vec<T, VB> u = ldv<T, VB>(b + jc[g] + n * (l0 + t));
 #pragma unroll
-                    for (int e = 0; e < VB; ++e) bv[g + e][t] = tmp[e];
+                    for (int e = 0; e < VB; ++e) bv[g + e][t] = u.v[e];
                 }
         }
 #pragma unroll
@@ -214,15 +242,14 @@ __device__ __forceinline__ void micro_tile(const T *__restrict__ a, const T *__r
         for (int g = 0; g < RM; g += VC) {
             if (!rv[g]) continue;
             const int i = ir[g];
-            T y[VC];
+            Vec<T, VC> y;
             if constexpr (B0) {
 #pragma unroll
-                for (int e = 0; e < VC; ++e) y[e] = ax(alpha, acc[g + e][c]);
+                for (int e = 0; e < VC; ++e) y.v[e] = ax(alpha, acc[g + e][c]);
             } else {
-                T x[VC];
-                ldv<T, VC>(cin + i + m * j, x);
+                const Vec<T, VC> x = ldv<T, VC>(cin + i + m * j);
 #pragma unroll
-                for (int e = 0; e < VC; ++e) y[e] = axpby(alpha, acc[g + e][c], beta, x[e]);
+                for (int e = 0; e < VC; ++e) y.v[e] = axpby(alpha, acc[g + e][c], beta, x.v[e]);
             }
             stv<T, VC>(cout + i + ldo * j, y);
         }
