@@ -127,12 +127,13 @@ def dist_setup(args):
 def make_inputs(rank, set_id, device):
     """Seeded synthetic batch for one rank: global pair indices [rank*BATCH, (rank+1)*BATCH)."""
     import txinputs
+    from paper_1304_7053_b200 import shard
 
     out = {}
     for n in SIZES:
         key = lambda name: txinputs.stream_key(txinputs.DEFAULT_SEED, "bench", set_id, KIND, n, name)
-        e = n * n
-        out[n] = tuple(txinputs.values_torch(KIND, key(nm), rank * BATCH * e, BATCH * e, device)
+        lo, hi = shard.element_range(shard.weak_range(BATCH, rank), n * n)
+        out[n] = tuple(txinputs.values_torch(KIND, key(nm), lo, hi - lo, device)
                        for nm in ("A", "B", "C"))
     return out
 

@@ -11,7 +11,8 @@
 //
 // Cost model: per warp instruction, lanes form phases of 128/bytes lanes; a
 // phase costs the max over the 32 banks of the distinct 4-byte words it
-// requests.  Score = wavefronts per pair (compute loads + C in + out stores),
+// requests.  Score = wavefronts per pair (compute loads + C in) + 128-byte
+// lines touched by the global C stores,
 // ties broken by instructions per pair, then registers.
 //
 //   g++ -O2 -std=c++17 -o /tmp/mapsearch tools/mapsearch.cpp && /tmp/mapsearch > ...
@@ -179,16 +180,32 @@ static Cost cost(const Inst &s, const Map &m, int P)
                     }
             }
         }
-        // epilogue: C is stored straight to global memory; only the beta != 0 C-in
-        // reads touch shared memory.
-        if (!s.b0)
-            for (int cc = 0; cc < m.RN; ++cc)
-                for (int r = 0; r < m.RM; r += m.VC) {
+        // epilogue: the beta != 0 C-in reads touch shared memory; C is stored straight
+        // to global memory, costed as the number of distinct 128-byte lines each store
+        // instruction touches (L1TEX wavefronts; fewer lines = better coalescing).
+        for (int cc = 0; cc < m.RN; ++cc)
+            for (int r = 0; r < m.RM; r += m.VC) {
+                if (!s.b0) {
                     for (int ln = 0; ln < 32; ++ln)
                         addr[ln] = (C0 + (long)q[ln] * SC + row(ln, r) + (long)M * col(ln, cc)) * wpe;
                     wf += wavefronts(addr, m.VC * wpe, act);
                     ++ni;
                 }
+                long lines[32];
+                int nl = 0;
+                for (int ln = 0; ln < 32; ++ln) {
+                    if (!act[ln]) continue;
+                    long b0 = ((long)q[ln] * SC + row(ln, r) + (long)M * col(ln, cc)) * s.es;
+                    for (long bb = b0 / 128; bb <= (b0 + m.VC * s.es - 1) / 128; ++bb) {
+                        bool seen = false;
+                        for (int t = 0; t < nl; ++t)
+                            if (lines[t] == bb) { seen = true; break; }
+                        if (!seen && nl < 32) lines[nl++] = bb;
+                    }
+                }
+                wf += nl;
+                ++ni;
+            }
     }
     c.wf = (double)wf / P;
     c.ninst = (double)ni / P;
