@@ -31,8 +31,9 @@
  *    and disjoint from the inputs (documented precondition, not checked: checking
  *    would need device reads).
  *
- * Memory and ownership.  The caller owns all memory; the library allocates none
- * on these calls.  A, B, C, the pointer arrays and their targets are device
+ * Memory and ownership.  The caller owns all memory; the library allocates no
+ * device memory (the host-buffer entry creates two copy streams per device once,
+ * and a few events per call).  A, B, C, the pointer arrays and their targets are device
  * memory of the CURRENT device.  alpha and beta are HOST pointers, read before
  * the call returns (the paper allows host or device; device
  * mode is out of scope, reading R12).
@@ -115,8 +116,11 @@ int tx_gemm_batched_ptr_z(char transa, char transb, int m, int n, int k,
  * same layouts (offsets and extents) as hA, hB, hC.  Enqueues on `stream`:
  * host->device copies of the A and B extents (and of C's extent when
  * beta != 0), the GEMM on the device copies, and the device->host copy of C's
- * extent back into hC.  The batch is processed in chunks so that copies of one
- * chunk overlap the GEMM of another.  Returns as the strided call; a NULL
+ * extent back into hC.  The batch is processed in chunks of ~32 MB: host->device
+ * copies run on an internal copy stream, device->host copies on another, the
+ * GEMMs on `stream`, ordered by events, so both PCIe directions and the kernels
+ * overlap; work already queued on `stream` is ordered before the first copy and
+ * `stream` is ordered after the last one.  Returns as the strided call; a NULL
  * staging buffer that would be used returns -19/-20/-21. ---- */
 int tx_gemm_batched_hostio_s(char transa, char transb, int m, int n, int k,
                              const float *alpha, const float *hA, int lda, long long lda2,

@@ -324,6 +324,29 @@ static int gemm_ptr(char ta, char tb, int m, int n, int k, const U *alpha, const
 }
 
 // ---------------------------------------------------------- host-buffer call
+// Auxiliary copy streams (one pair per device, created once): host->device copies
+// run on one, device->host on the other, the GEMM chunks on the caller's stream,
+// ordered by events, so PCIe transfers in both directions overlap each other and
+// the kernels.
+struct CopyStreams {
+    cudaStream_t h2d = nullptr, d2h = nullptr;
+};
+static CopyStreams copy_streams()
+{
+    static std::mutex mu;
+    static CopyStreams per_dev[64];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) dev = 0;
+    std::lock_guard<std::mutex> g(mu);
+    CopyStreams &c = per_dev[dev];
+    if (!c.h2d) {
+        cudaStreamCreateWithFlags(&c.h2d, cudaStreamNonBlocking);
+        cudaStreamCreateWithFlags(&c.d2h, cudaStreamNonBlocking);
+    }
+    return c;
+}
+
 template <class U>
 static int gemm_hostio(char ta, char tb, int m, int n, int k, const U *alpha, const U *hA, int lda,
                        long long lda2, const U *hB, int ldb, long long ldb2, const U *beta, U *hC,
@@ -347,22 +370,69 @@ static int gemm_hostio(char ta, char tb, int m, int n, int k, const U *alpha, co
     const int rowsA = op_n(ta) ? m : k, colsA = op_n(ta) ? k : m;
     const int rowsB = op_n(tb) ? k : n, colsB = op_n(tb) ? n : k;
     const size_t es = sizeof(U);
-    const long long eA = extent_elems(rowsA, colsA, lda, lda2, batch);
-    const long long eB = extent_elems(rowsB, colsB, ldb, ldb2, batch);
-    const long long eC = extent_elems(m, n, ldc, ldc2, batch);
+    const bool read_c = !AT::zero(b);
+    // Chunks of whole pairs (~32 MB of traffic each); ld2 == 0 operands are copied once.
+    const long long per_pair = (long long)es * ((reads_ab ? lda2 + ldb2 : 0) + ldc2 * (read_c ? 2 : 1));
+    long long chunk = per_pair > 0 ? (32ll << 20) / per_pair : batch;
+    if (chunk < 1) chunk = 1;
+    const int nchunks = (int)((batch + chunk - 1) / chunk);
+    CopyStreams cs = copy_streams();
+    cudaEvent_t ev0;
+    cudaEventCreateWithFlags(&ev0, cudaEventDisableTiming);
+    cudaEventRecord(ev0, st);
+    cudaStreamWaitEvent(cs.h2d, ev0, 0);
+    cudaStreamWaitEvent(cs.d2h, ev0, 0);
+    cudaEventDestroy(ev0);
     cudaError_t e = cudaSuccess;
-    if (reads_ab) {
-        e = cudaMemcpyAsync(dA, hA, eA * es, cudaMemcpyHostToDevice, st);
-        if (e == cudaSuccess) e = cudaMemcpyAsync(dB, hB, eB * es, cudaMemcpyHostToDevice, st);
+    int launches = 0, path = PATH_NONE;
+    for (int c = 0; c < nchunks && e == cudaSuccess; ++c) {
+        const long long p0 = (long long)c * chunk;
+        const int nb = (int)(batch - p0 < chunk ? batch - p0 : chunk);
+        const long long oa = lda2 * p0, ob = ldb2 * p0, oc = ldc2 * p0;
+        if (reads_ab) {
+            if (c == 0 || lda2 != 0)
+                e = cudaMemcpyAsync(dA + oa, hA + oa, extent_elems(rowsA, colsA, lda, lda2, nb) * es,
+                                    cudaMemcpyHostToDevice, cs.h2d);
+            if (e == cudaSuccess && (c == 0 || ldb2 != 0))
+                e = cudaMemcpyAsync(dB + ob, hB + ob, extent_elems(rowsB, colsB, ldb, ldb2, nb) * es,
+                                    cudaMemcpyHostToDevice, cs.h2d);
+        }
+        const long long ec = extent_elems(m, n, ldc, ldc2, nb);
+        if (e == cudaSuccess && read_c)
+            e = cudaMemcpyAsync(dC + oc, hC + oc, ec * es, cudaMemcpyHostToDevice, cs.h2d);
+        cudaEvent_t ein, ek;
+        cudaEventCreateWithFlags(&ein, cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&ek, cudaEventDisableTiming);
+        cudaEventRecord(ein, cs.h2d);
+        cudaStreamWaitEvent(st, ein, 0);
+        if (e == cudaSuccess) {
+            rc = gemm_strided<U>(ta, tb, m, n, k, alpha, dA + oa, lda, lda2, dB + ob, ldb, ldb2,
+                                 beta, dC + oc, ldc, ldc2, nb, st);
+            if (rc) {
+                cudaEventDestroy(ein);
+                cudaEventDestroy(ek);
+                return rc;
+            }
+            launches += t_last_launches;
+            path = t_last_path;
+        }
+        cudaEventRecord(ek, st);
+        cudaStreamWaitEvent(cs.d2h, ek, 0);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(hC + oc, dC + oc, ec * es, cudaMemcpyDeviceToHost, cs.d2h);
+        cudaEventDestroy(ein);
+        cudaEventDestroy(ek);
     }
-    if (e == cudaSuccess && !AT::zero(b))
-        e = cudaMemcpyAsync(dC, hC, eC * es, cudaMemcpyHostToDevice, st);
+    // the caller's stream is ordered after the last device->host copy
+    cudaEvent_t eend;
+    cudaEventCreateWithFlags(&eend, cudaEventDisableTiming);
+    cudaEventRecord(eend, cs.d2h);
+    cudaStreamWaitEvent(st, eend, 0);
+    cudaEventDestroy(eend);
     if (e != cudaSuccess) return as_status(e);
-    rc = gemm_strided<U>(ta, tb, m, n, k, alpha, dA, lda, lda2, dB, ldb, ldb2, beta, dC, ldc, ldc2,
-                         batch, st);
-    if (rc) return rc;
-    e = cudaMemcpyAsync(hC, dC, eC * es, cudaMemcpyDeviceToHost, st);
-    return as_status(e);
+    t_last_path = path;
+    t_last_launches = launches;
+    return 0;
 }
 
 }  // namespace tx

@@ -301,6 +301,8 @@ __global__ void __launch_bounds__(NT) bulk_kernel(const Params<T> p)
         fence_mbar_init();
     }
     __syncthreads();
+    grid_dep_wait();    // PDL: the prologue above overlapped the previous grid's tail
+    grid_dep_launch();
 
     auto issue = [&](int i) {  // local tile i -> stage i % S (thread 0 only)
         const long long pair0 = (blockIdx.x + (long long)i * G) * P;
@@ -390,6 +392,8 @@ __global__ void __launch_bounds__(NT) gather_kernel(const Params<T> p)
         }
     };
 
+    grid_dep_wait();
+    grid_dep_launch();
     for (int i = 0; i < GS - 1; ++i) {
         if (i < my_tiles) issue(i);
         cp_async_commit();
@@ -438,6 +442,8 @@ __device__ __forceinline__ double2 scal(double2 b, double2 y)
 template <class T, bool PTR, bool B0>
 __global__ void __launch_bounds__(256) scale_kernel(const Params<T> p)
 {
+    grid_dep_wait();
+    grid_dep_launch();
     const long long mn = (long long)p.m * p.n;
     const long long total = mn * p.batch;
     for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
