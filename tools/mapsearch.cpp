@@ -231,8 +231,7 @@ int main(int argc, char **argv)
     } types[] = {{"float", 4, false}, {"double", 8, false}, {"float2", 8, true}, {"double2", 16, true}};
     int only_n = argc > 1 ? atoi(argv[1]) : 0;
     printf("// Generated by tools/mapsearch.cpp -- do not edit.  Columns:\n");
-    printf("// TX_MAP(T, n, OPA, OPB, B0, RM, RN, RMODE, CMODE, LO, VA, VB, VC, ROTN) "
-           "// wavefronts/pair, insts/pair, est. regs, baseline(4x4) wavefronts\n");
+    printf("// TX_MAP(T, n, OPA, OPB, B0, RM, RN, RMODE, CMODE, LO, VA, VB, VC, ROTN, S)\n");
     for (auto &t : types) {
         const int wpe = t.es / 4;
         const int acc_cap = 64;  // accumulator registers per thread
@@ -245,42 +244,66 @@ int main(int argc, char **argv)
                         Inst s{t.es, n, n, n, *pa == 'N' ? 'N' : 'T', *pb == 'N' ? 'N' : 'T', b0 == 1};
                         Map bestm{};
                         Cost bestc{1e18, 1e18, 0};
+                        double best_t = 1e18;
+                        int best_S = 4;
                         std::vector<int> rms, rns;
                         for (int b = 1; b <= n; ++b) {
                             int r = (n + b - 1) / b;
                             if (rms.empty() || rms.back() != r) rms.push_back(r);
                         }
                         rns = rms;
-                        // occupancy floor: a 128-thread CTA computes on 128/tpm pairs per
-                        // stage; 2 CTAs per SM with 4 stages each must fit in ~110 KB, so a
-                        // stage holds at most 27 KB: tpm >= 128 * in_bytes / 27 KB.
                         const int in_bytes = (n * n * 2 + (b0 ? 0 : n * n)) * t.es;
-                        int tpm_min = (int)((128L * in_bytes + 27647) / 27648);
-                        if (tpm_min > n * n) tpm_min = n * n;
+                        const double pair_bytes = (double)(n * n * (b0 ? 3 : 4)) * t.es;
+                        const int cm = t.cplx ? 4 : 1;          // real FMAs per complex MAC
+                        const double fp_rate = t.es == 8 && !t.cplx ? 64.0 : (t.es == 16 ? 64.0 : 128.0);
                         for (int RM : rms)
                             for (int RN : rns) {
                                 if (RM * RN * wpe > acc_cap) continue;
                                 const int tpm = blocks(n, RM) * blocks(n, RN);
-                                if (tpm > 128 || tpm < tpm_min) continue;
+                                if (tpm > 128) continue;
                                 const int P = pairs_for(s, tpm);
-                                for (int RMODE = 0; RMODE < 2; ++RMODE)
-                                    for (int CMODE = 0; CMODE < 2; ++CMODE)
-                                        for (int LO = 0; LO < 2; ++LO)
-                                            for (int VA : {1, 2, 4})
-                                                for (int VB : {1, 2, 4})
-                                                    for (int VC : {1, 2, 4})
-                                                        for (int ROTN : {0, 1, 2, 3, 4}) {
-                                                            Map m{RM, RN, RMODE, CMODE, LO, VA, VB, VC, ROTN};
-                                                            if (!valid(s, m)) continue;
-                                                            Cost c = cost(s, m, P);
-                                                            // fewest wavefronts; then instructions; then regs
-                                                            double key = c.wf + 0.02 * c.ninst + 0.0001 * c.regs;
-                                                            double bkey = bestc.wf + 0.02 * bestc.ninst + 0.0001 * bestc.regs;
-                                                            if (key < bkey - 1e-9) {
-                                                                bestc = c;
-                                                                bestm = m;
+                                for (int S = 2; S <= 4; ++S) {
+                                    // the runtime planner (tx_dispatch.cuh plan_tiles): P = one
+                                    // 128-thread pass x enough passes for a ~16 KB stage
+                                    const int ppass = std::max(1, 128 / tpm);
+                                    const int passes = std::max(1, 16384 / (ppass * in_bytes));
+                                    const long stage = (long)ppass * passes * in_bytes;
+                                    const int ctas = (int)std::min<long>(16, (225 * 1024L) / (S * stage + 64));
+                                    if (ctas < 2) continue;
+                                    const double warps = ctas * std::min(128, ppass * tpm) / 32.0;
+                                    for (int RMODE = 0; RMODE < 2; ++RMODE)
+                                        for (int CMODE = 0; CMODE < 2; ++CMODE)
+                                            for (int LO = 0; LO < 2; ++LO)
+                                                for (int VA : {1, 2, 4})
+                                                    for (int VB : {1, 2, 4})
+                                                        for (int VC : {1, 2, 4})
+                                                            for (int ROTN : {0, 1, 2, 3, 4}) {
+                                                                Map m{RM, RN, RMODE, CMODE, LO, VA, VB, VC, ROTN};
+                                                                if (!valid(s, m)) continue;
+                                                                Cost c = cost(s, m, P);
+                                                                // ---- predicted cycles per pair per SM
+                                                                const double macs = (double)tpm * RM * RN * n * cm;
+                                                                const double t_hbm = pair_bytes / 20.5;
+                                                                const double t_smem = c.wf + in_bytes / 128.0;
+                                                                const double t_fp = macs / fp_rate;
+                                                                // calibrated on ncu (r01): ~2.2 warp-instructions per
+                                                                // clock per SM at 8-12 warps; per-item overhead ~40 +
+                                                                // epilogue ~6 (12 complex) instructions per output
+                                                                const double other = c.ninst + tpm * (60.0 + 3.0 * (RM + RN) + 7.0 * RM * RN * (t.cplx ? 2 : 1)) / 32.0;
+                                                                const double eff = std::min(1.0, warps / 8.0) * 0.55;
+                                                                const double t_issue = (macs / 32.0 + other) / (4.0 * eff);
+                                                                // fewer stages than 3 exposes DRAM latency between tiles
+                                                                const double t_pipe = t_hbm * (S == 2 ? 1.25 : (S == 3 ? 1.05 : 1.0));
+                                                                const double tp = std::max(std::max(t_pipe, t_smem), std::max(t_fp, t_issue));
+                                                                const double key = tp + 0.001 * c.wf + 0.0001 * c.regs;
+                                                                if (key < best_t - 1e-9) {
+                                                                    best_t = key;
+                                                                    bestc = c;
+                                                                    bestm = m;
+                                                                    best_S = S;
+                                                                }
                                                             }
-                                                        }
+                                }
                             }
                         int r4 = std::min(4, n);
                         int r4b = blocks(n, blocks(n, r4));
@@ -288,11 +311,12 @@ int main(int argc, char **argv)
                         Cost bc = cost(s, base, pairs_for(s, blocks(n, r4b) * blocks(n, r4b)));
                         int opa = *pa == 'N' ? 0 : (*pa == 'T' ? 1 : 2);
                         int opb = *pb == 'N' ? 0 : (*pb == 'T' ? 1 : 2);
-                        printf("TX_MAP(%s, %d, %d, %d, %d, %d, %d, %d, %d, %d, %d, %d, %d, %d) "
-                               "// %.1f %.1f %d base %.1f\n",
+                        printf("TX_MAP(%s, %d, %d, %d, %d, %d, %d, %d, %d, %d, %d, %d, %d, %d, %d) "
+                               "// wf %.1f inst %.1f regs %d pred %.0f clk/pair hbm %.0f (base wf %.1f)\n",
                                t.name, n, opa, opb, b0, bestm.RM, bestm.RN, bestm.RMODE,
                                bestm.CMODE, bestm.LO, bestm.VA, bestm.VB, bestm.VC, bestm.ROTN,
-                               bestc.wf, bestc.ninst, bestc.regs, bc.wf);
+                               best_S, bestc.wf, bestc.ninst, bestc.regs, best_t,
+                               (double)(n * n * (b0 ? 3 : 4)) * t.es / 20.5, bc.wf);
                         fflush(stdout);
                     }
         }
