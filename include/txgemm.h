@@ -160,6 +160,10 @@ int tx_last_path(int *launches);
  * depend on it; used for the grid-sweep experiment and determinism tests.
  * Process-wide; returns the previous value. */
 int tx_set_max_ctas(int max_ctas);
+/* Autotuning hook: force the bulk kernels' pipeline depth (2..8 stages) and
+ * stage-size target (KB); 0 restores the per-instance table.  Process-wide;
+ * returns the previous stage override.  Results do not depend on it. */
+int tx_set_tuning(int stages, int stage_kb);
 /* Number of compiled kernel instances (AOT, size-specialised + generic). */
 int tx_num_instances(void);
 

@@ -84,6 +84,8 @@ def lib():
         L.tx_set_max_ctas.argtypes = [ci]
         L.tx_set_max_ctas.restype = ci
         L.tx_num_instances.restype = ci
+        L.tx_set_tuning.argtypes = [ci, ci]
+        L.tx_set_tuning.restype = ci
         _lib = L
         return L
 
@@ -143,6 +145,11 @@ def last_path():
 
 def set_max_ctas(v: int) -> int:
     return lib().tx_set_max_ctas(int(v))
+
+
+def set_tuning(stages: int = 0, stage_kb: int = 0) -> int:
+    """Autotuning hook (tx_set_tuning): force pipeline depth / stage size; 0, 0 resets."""
+    return lib().tx_set_tuning(int(stages), int(stage_kb))
 
 
 def num_instances() -> int:

@@ -60,6 +60,9 @@ TypeTables &tables(int t)
 
 static std::atomic<int> g_max_ctas{0};
 int max_ctas_override() { return g_max_ctas.load(std::memory_order_relaxed); }
+static std::atomic<int> g_tune_stages{0}, g_tune_kb{0};
+int tune_stages() { return g_tune_stages.load(std::memory_order_relaxed); }
+int tune_stage_bytes() { return g_tune_kb.load(std::memory_order_relaxed) * 1024; }
 
 int num_sms()
 {
@@ -498,6 +501,14 @@ extern "C" int tx_last_path(int *launches)
 }
 
 extern "C" int tx_set_max_ctas(int v) { return g_max_ctas.exchange(v < 0 ? 0 : v); }
+
+extern "C" int tx_set_tuning(int stages, int stage_kb)
+{
+    const int prev = g_tune_stages.load();
+    g_tune_stages.store(stages >= 2 && stages <= 8 ? stages : 0);
+    g_tune_kb.store(stage_kb > 0 && stage_kb <= 96 ? stage_kb : 0);
+    return prev;
+}
 
 extern "C" int tx_num_instances(void)
 {

@@ -56,16 +56,17 @@ struct Params {
 //   lanes rb fastest (LO 0) | cb fastest (LO 1)
 //   VA/VB/VC: vector width (elements) of the shared-memory accesses of A, B
 //         and C along their stored-contiguous dimension.
-//   S:    pipeline stages the planner should use.
+//   S, KB: pipeline stages and stage-size target the planner uses (autotuned).
 // Every mapping accumulates each output over l = 0..k-1 in ascending order, so
 // all mappings (and the gather / pointer paths) give bitwise-identical results.
 // --------------------------------------------------------------------------
 template <int RM_, int RN_, int RMODE_, int CMODE_, int LO_, int VA_, int VB_, int VC_, int ROTN_,
-          int S_ = 0>
+          int S_ = 0, int KB_ = 0>
 struct MapT {
     static constexpr int RM = RM_, RN = RN_, RMODE = RMODE_, CMODE = CMODE_, LO = LO_;
     static constexpr int VA = VA_, VB = VB_, VC = VC_, ROTN = ROTN_;
-    static constexpr int S = S_;  // pipeline stages (0 = planner's choice)
+    static constexpr int S = S_;    // pipeline stages (0 = planner's choice)
+    static constexpr int KB = KB_;  // stage-size target in KB (0 = default 16)
 };
 
 // Vector shared/global accesses of V consecutive elements, moved element by
