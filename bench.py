@@ -120,7 +120,7 @@ def dist_setup(args):
         import torch.distributed as dist
 
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl")
+        dist.init_process_group(args.dist_backend)
     return world, rank, local
 
 
@@ -256,12 +256,21 @@ def run_reference(args, world, rank):
     print(json.dumps(line), flush=True)
 
 
+def max_over_ranks(v, dev, args):
+    import torch
+
+    t = torch.tensor([v], device=dev if args.dist_backend == "nccl" else "cpu")
+    torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    return float(t.item())
+
+
 def run_ours(args, world, rank, local):
     import torch
 
     import paper_1304_7053_b200 as tx
     from paper_1304_7053_b200 import model
 
+    local = local % torch.cuda.device_count()  # several ranks per GPU only when testing (gloo)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     tx.lib()  # fails loudly if the CUDA library is missing: no fallback
@@ -333,9 +342,7 @@ def run_ours(args, world, rank, local):
     clocks = clk.stop(t_wall0, t_wall1)
     evented = {n: statistics.mean(a.elapsed_time(b) for m_, a, b in evs if m_ == n) for n in SIZES}
     if world > 1:
-        t = torch.tensor([ms], device=dev)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ms = float(t.item())
+        ms = max_over_ranks(ms, dev, args)
 
     flops_step = sum(model.flops(KIND, n, n, n, BATCH) for n in SIZES)
     bytes_step = sum(model.bytes_moved(KIND, n, n, n, BATCH, True, True) for n in SIZES)
@@ -385,9 +392,7 @@ def run_ours(args, world, rank, local):
         torch.cuda.synchronize()
         ems = s0.elapsed_time(s1)
         if world > 1:
-            t = torch.tensor([ems], device=dev)
-            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-            ems = float(t.item())
+            ems = max_over_ranks(ems, dev, args)
         e2e = {"value": round(flops_step * KE * world / (ems / 1e3) / 1e9, 2), "unit": "GFlop/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": KE,
                "api": "tx_gemm_batched_hostio_s (host buffers, copies inside the timed region)"}
@@ -422,6 +427,9 @@ def main():
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--dist-backend", default="nccl", choices=("nccl", "gloo"),
+                    help="process-group backend for the barrier / max-over-ranks (gloo: testing "
+                         "several ranks on one GPU)")
     args = ap.parse_args()
     world, rank, local = dist_setup(args)
     if args.impl == "reference":

@@ -24,6 +24,7 @@ L2 = 126 * 1024 * 1024
 def run_case(kind, m, n, k, batch, ta, tb, general, reps, peak, layout="strided"):
     es = model.ESIZE[kind]
     per_set = es * (m * k + k * n + m * n) * batch
+    ptr = layout == "ptr"
     R = max(1, min(8, -(-4 * L2 // per_set)))
     sets = []
     for r in range(R):
@@ -37,10 +38,23 @@ def run_case(kind, m, n, k, batch, ta, tb, general, reps, peak, layout="strided"
     lda = m if ta in "nN" else k
     ldb = k if tb in "nN" else n
 
+    if ptr:  # pointer arrays in a seeded random order (BASELINE configs[3])
+        perm = torch.randperm(batch, generator=torch.Generator().manual_seed(3)).cuda()
+        psets = []
+        for A, B, C in sets:
+            e = A.element_size()
+            psets.append((A.data_ptr() + perm * (m * k * e), B.data_ptr() + perm * (k * n * e),
+                          C.data_ptr() + perm * (m * n * e)))
+
     def call(s):
-        A, B, C = s
-        rc = tx.tx_gemm_batched(kind, ta, tb, m, n, k, alpha, A, lda, m * k, B, ldb, k * n, beta,
-                                C, m, m * n, batch)
+        if ptr:
+            pa, pb, pc = psets[sets.index(s)]
+            rc = tx.tx_gemm_batched_ptr(kind, ta, tb, m, n, k, alpha, pa, lda, pb, ldb, beta, pc,
+                                        m, batch)
+        else:
+            A, B, C = s
+            rc = tx.tx_gemm_batched(kind, ta, tb, m, n, k, alpha, A, lda, m * k, B, ldb, k * n,
+                                    beta, C, m, m * n, batch)
         assert rc == 0, tx.status_string(rc)
 
     for i in range(2 * R):
@@ -54,12 +68,15 @@ def run_case(kind, m, n, k, batch, ta, tb, general, reps, peak, layout="strided"
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / reps
     byts = model.bytes_moved(kind, m, n, k, batch, True, general)
+    if ptr:
+        byts_ptr = model.bytes_moved(kind, m, n, k, batch, True, general, pointer_arrays=True)
     gbps = byts / (ms / 1e3) / 1e9
     return {"kind": kind, "m": m, "n": n, "k": k, "ops": ta + tb, "beta0": not general,
             "batch": batch, "us": round(ms * 1e3, 2), "gbps": round(gbps, 1),
             "frac_measured": round(gbps / peak, 4),
             "gflops": round(model.flops(kind, m, n, k, batch) / (ms / 1e3) / 1e9, 1),
-            "path": tx.last_path()[0], "sets": R}
+            "path": tx.last_path()[0], "sets": R, "layout": layout,
+            **({"gbps_with_pointers": round(byts_ptr / (ms / 1e3) / 1e9, 1)} if ptr else {})}
 
 
 def main():
@@ -70,11 +87,28 @@ def main():
     ap.add_argument("--ops", default="NN")
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--out", default="")
+    ap.add_argument("--shapes", default="", help="m x n x k list, e.g. 8x16x4,16x3x16")
+    ap.add_argument("--layout", default="strided", choices=("strided", "ptr"))
     a = ap.parse_args()
     lo, hi = (int(x) for x in a.sizes.split("-")) if "-" in a.sizes else (int(a.sizes),) * 2
     peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
     out = open(a.out, "w") if a.out else None
     ops = a.ops.split(",")
+    if a.shapes:
+        for kind in a.kinds:
+            for shp in a.shapes.split(","):
+                m, n, k = (int(x) for x in shp.split("x"))
+                for op in ops:
+                    if kind in "sd" and "C" in op:
+                        continue
+                    for general in (False, True):
+                        r = run_case(kind, m, n, k, a.batch, op[0], op[1], general, a.reps, peak,
+                                     a.layout)
+                        print(json.dumps(r), flush=True)
+                        if out:
+                            out.write(json.dumps(r) + "\n")
+                        torch.cuda.empty_cache()
+        return
     for kind in a.kinds:
         for nn in range(lo, hi + 1):
             for op in ops:
