@@ -152,9 +152,10 @@ const char *tx_status_string(int status);
 int tx_version(void);
 /* Path the calling thread's most recent successful GEMM call took:
  * 0 none/quick return, 1 packed bulk-copy (TMA) kernel, 2 general gather kernel,
- * 3 pointer-array gather kernel, 4 scale-only kernel (alpha == 0 or k == 0);
- * +16 when a separate tail launch handled the last (< 16) pairs.  Also
- * returns the number of kernel launches of that call in *launches. */
+ * 3 pointer-array kernel, 4 scale-only kernel (alpha == 0 or k == 0);
+ * +16 when a separate tail launch handled the last (< 16) pairs; +32 when the
+ * kernel was a runtime-specialised (NVRTC, sm_100a) instance.  Also returns
+ * the number of kernel launches of that call in *launches. */
 int tx_last_path(int *launches);
 /* Cap on CTAs per launch (0 = automatic: SMs x resident CTAs).  Results do not
  * depend on it; used for the grid-sweep experiment and determinism tests.
@@ -164,6 +165,14 @@ int tx_set_max_ctas(int max_ctas);
  * stage-size target (KB); 0 restores the per-instance table.  Process-wide;
  * returns the previous stage override.  Results do not depend on it. */
 int tx_set_tuning(int stages, int stage_kb);
+/* Runtime specialisation (NVRTC) of instances without an ahead-of-time kernel
+ * (non-square sizes, pointer arrays, padded layouts): 1 enables (default, unless
+ * TX_JIT=0 in the environment), 0 uses the generic-size AOT kernels.  Results are
+ * bitwise identical either way.  Returns the previous setting. */
+int tx_set_jit(int enable);
+/* Number of instances JIT-compiled by this process (cache misses), or -1 when
+ * NVRTC is unavailable. */
+int tx_jit_compiled(void);
 /* Number of compiled kernel instances (AOT, size-specialised + generic). */
 int tx_num_instances(void);
 

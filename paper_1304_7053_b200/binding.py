@@ -23,7 +23,8 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libtxgemm.so")
 
 KINDS = ("s", "d", "c", "z")
-PATHS = {0: "none", 1: "bulk", 2: "gather", 3: "ptr", 4: "scale", 17: "bulk+tail"}
+PATHS = {0: "none", 1: "bulk", 2: "gather", 3: "ptr", 4: "scale", 17: "bulk+tail",
+         33: "bulk", 34: "gather", 35: "ptr", 49: "bulk+tail"}
 
 
 class TxError(RuntimeError):
@@ -86,6 +87,9 @@ def lib():
         L.tx_num_instances.restype = ci
         L.tx_set_tuning.argtypes = [ci, ci]
         L.tx_set_tuning.restype = ci
+        L.tx_set_jit.argtypes = [ci]
+        L.tx_set_jit.restype = ci
+        L.tx_jit_compiled.restype = ci
         _lib = L
         return L
 
@@ -141,6 +145,19 @@ def last_path():
     n = ctypes.c_int(0)
     p = lib().tx_last_path(ctypes.byref(n))
     return PATHS.get(p, str(p)), n.value
+
+
+def last_path_jit() -> bool:
+    """True when the most recent call ran a runtime-specialised (NVRTC) instance."""
+    return bool(lib().tx_last_path(None) & 32)
+
+
+def set_jit(enable: bool) -> int:
+    return lib().tx_set_jit(1 if enable else 0)
+
+
+def jit_compiled() -> int:
+    return lib().tx_jit_compiled()
 
 
 def set_max_ctas(v: int) -> int:

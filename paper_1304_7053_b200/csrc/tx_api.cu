@@ -14,6 +14,7 @@
 
 #include "txgemm.h"
 #include "tx_dispatch.cuh"
+#include "tx_jit.h"
 
 namespace tx {
 
@@ -250,11 +251,15 @@ static int gemm_strided(char ta, char tb, int m, int n, int k, const U *alpha, c
             q.ldb2 = SB;
             q.ldc2 = SC;
             LaunchFn fn = (m == n && n == k) ? tab.bulk_sq[opa][opb][b0][m - 1] : nullptr;
-            if (!fn) fn = tab.bulk_dyn[opa][opb][b0];
-            const cudaError_t e = fn(&q, st);
+            cudaError_t e = cudaErrorNotSupported;
+            path = PATH_BULK;
+            if (!fn) {  // no AOT instance for this shape: runtime-specialised instance
+                e = launch_jit<T>(JIT_BULK, q, opa, opb, b0, st);
+                if (e == cudaSuccess) path |= PATH_JIT;
+            }
+            if (e == cudaErrorNotSupported) e = (fn ? fn : tab.bulk_dyn[opa][opb][b0])(&q, st);
             if (e != cudaSuccess) return as_status(e);
             ++launches;
-            path = PATH_BULK;
         }
         if (main_pairs < batch) {  // < 16 trailing pairs whose bytes are not 16-aligned
             Params<T> q = p;
@@ -268,10 +273,12 @@ static int gemm_strided(char ta, char tb, int m, int n, int k, const U *alpha, c
             const cudaError_t e = tab.gather[opa][opb][b0][0](&q, st);
             if (e != cudaSuccess) return as_status(e);
             ++launches;
-            path = main_pairs > 0 ? (PATH_BULK | PATH_TAIL) : PATH_GATHER;
+            path = main_pairs > 0 ? (path | PATH_TAIL) : PATH_GATHER;
         }
     } else {
-        const cudaError_t e = tab.gather[opa][opb][b0][0](&p, st);
+        cudaError_t e = launch_jit<T>(JIT_GATHER, p, opa, opb, b0, st);
+        if (e == cudaSuccess) path |= PATH_JIT;
+        if (e == cudaErrorNotSupported) e = tab.gather[opa][opb][b0][0](&p, st);
         if (e != cudaSuccess) return as_status(e);
         launches = 1;
     }
@@ -318,8 +325,15 @@ static int gemm_ptr(char ta, char tb, int m, int n, int k, const U *alpha, const
         e = tab.scale[1][b0](&p, st);
         t_last_path = PATH_SCALE;
     } else {
-        e = tab.gather[op_code(ta, AT::cplx)][op_code(tb, AT::cplx)][b0][1](&p, st);
-        t_last_path = PATH_PTR;
+        const int opa = op_code(ta, AT::cplx), opb = op_code(tb, AT::cplx);
+        const int rowsA = op_n(ta) ? m : k, rowsB = op_n(tb) ? k : n;
+        const int es = (int)sizeof(U);
+        // packed matrices whose byte sizes are multiples of 16: per-matrix bulk copies
+        const bool bulk_ok = lda == rowsA && ldb == rowsB && ldc == m && (m * k * es) % 16 == 0 &&
+                             (k * n * es) % 16 == 0 && (m * n * es) % 16 == 0;
+        e = launch_jit<T>(bulk_ok ? JIT_BULK_PTR : JIT_GATHER_PTR, p, opa, opb, b0, st);
+        t_last_path = PATH_PTR | (e == cudaSuccess ? PATH_JIT : 0);
+        if (e == cudaErrorNotSupported) e = tab.gather[opa][opb][b0][1](&p, st);
     }
     if (e != cudaSuccess) return as_status(e);
     t_last_launches = 1;
@@ -509,6 +523,10 @@ extern "C" int tx_set_tuning(int stages, int stage_kb)
     g_tune_kb.store(stage_kb > 0 && stage_kb <= 96 ? stage_kb : 0);
     return prev;
 }
+
+extern "C" int tx_set_jit(int enable) { return jit_set_enabled(enable); }
+
+extern "C" int tx_jit_compiled(void) { return jit_available() ? jit_compiled_count() : -1; }
 
 extern "C" int tx_num_instances(void)
 {

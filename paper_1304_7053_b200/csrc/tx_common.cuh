@@ -2,17 +2,25 @@
 // PTX wrappers (bulk async copies, mbarriers, cp.async) used by the kernels.
 #pragma once
 
+#ifndef __CUDACC_RTC__
 #include <cuda_runtime.h>
 #include <stdint.h>
+#else  // NVRTC (runtime specialisation, tx_jit.cu): no host headers
+typedef unsigned int uint32_t;
+typedef unsigned long long uint64_t;
+#endif
 
 namespace tx {
+
+template <class A, class B> struct same_t { static constexpr bool value = false; };
+template <class A> struct same_t<A, A> { static constexpr bool value = true; };
 
 // Operation codes for op(X).  For real types 'C' maps to OP_T.
 enum { OP_N = 0, OP_T = 1, OP_C = 2 };
 
 // Path codes reported by tx_last_path() (include/txgemm.h).
 enum { PATH_NONE = 0, PATH_BULK = 1, PATH_GATHER = 2, PATH_PTR = 3, PATH_SCALE = 4,
-       PATH_TAIL = 16 };
+       PATH_TAIL = 16, PATH_JIT = 32 };
 
 template <class T> struct is_cplx { static constexpr bool value = false; };
 template <> struct is_cplx<float2> { static constexpr bool value = true; };

@@ -23,9 +23,11 @@
 //    written straight from registers.
 #pragma once
 
-#include <type_traits>
-
+#ifndef __CUDACC_RTC__
 #include "tx_common.cuh"
+#else
+typedef unsigned long long uintptr_t;
+#endif
 
 namespace tx {
 
@@ -83,16 +85,16 @@ __device__ __forceinline__ Vec<T, V> ldv(const T *p)
     Vec<T, V> r;
     if constexpr (V == 1) {
         r.v[0] = *p;
-    } else if constexpr (std::is_same<T, float>::value && V == 4) {
+    } else if constexpr (same_t<T, float>::value && V == 4) {
         const float4 u = *reinterpret_cast<const float4 *>(p);
         r.v[0] = u.x; r.v[1] = u.y; r.v[2] = u.z; r.v[3] = u.w;
-    } else if constexpr (std::is_same<T, float>::value && V == 2) {
+    } else if constexpr (same_t<T, float>::value && V == 2) {
         const float2 u = *reinterpret_cast<const float2 *>(p);
         r.v[0] = u.x; r.v[1] = u.y;
-    } else if constexpr (std::is_same<T, double>::value && V == 2) {
+    } else if constexpr (same_t<T, double>::value && V == 2) {
         const double2 u = *reinterpret_cast<const double2 *>(p);
         r.v[0] = u.x; r.v[1] = u.y;
-    } else if constexpr (std::is_same<T, float2>::value && V == 2) {
+    } else if constexpr (same_t<T, float2>::value && V == 2) {
         const float4 u = *reinterpret_cast<const float4 *>(p);
         r.v[0] = make_float2(u.x, u.y); r.v[1] = make_float2(u.z, u.w);
     } else {
@@ -106,13 +108,13 @@ __device__ __forceinline__ void stv(T *p, const Vec<T, V> &r)
 {
     if constexpr (V == 1) {
         *p = r.v[0];
-    } else if constexpr (std::is_same<T, float>::value && V == 4) {
+    } else if constexpr (same_t<T, float>::value && V == 4) {
         *reinterpret_cast<float4 *>(p) = make_float4(r.v[0], r.v[1], r.v[2], r.v[3]);
-    } else if constexpr (std::is_same<T, float>::value && V == 2) {
+    } else if constexpr (same_t<T, float>::value && V == 2) {
         *reinterpret_cast<float2 *>(p) = make_float2(r.v[0], r.v[1]);
-    } else if constexpr (std::is_same<T, double>::value && V == 2) {
+    } else if constexpr (same_t<T, double>::value && V == 2) {
         *reinterpret_cast<double2 *>(p) = make_double2(r.v[0], r.v[1]);
-    } else if constexpr (std::is_same<T, float2>::value && V == 2) {
+    } else if constexpr (same_t<T, float2>::value && V == 2) {
         *reinterpret_cast<float4 *>(p) = make_float4(r.v[0].x, r.v[0].y, r.v[1].x, r.v[1].y);
     } else {
         static_assert(V == 1, "unsupported vector width");
@@ -347,17 +349,129 @@ __global__ void __launch_bounds__(NT) bulk_kernel(const Params<T> p)
 }
 
 // --------------------------------------------------------------------------
+// Pointer-array batches of packed matrices (ld = rows) whose byte sizes are
+// multiples of 16: per-matrix bulk async copies into the same S-stage mbarrier
+// ring, issued by the 32 lanes of warp 0 (lane q copies matrices q, q+32, ...),
+// with the tile's pointers prefetched one iteration ahead so the pointer loads
+// never stall the issue.  A matrix whose pointer is not 16-byte aligned is
+// copied synchronously by its lane instead (ordered before its use by the
+// end-of-iteration barrier; its bytes are excluded from the expected count).
+// P <= 32 * PPL pairs per tile.
+// --------------------------------------------------------------------------
+template <class T, int MS, int NS, int KS, int OPA, int OPB, bool B0, class MP, int NT>
+__global__ void __launch_bounds__(NT) bulk_ptr_kernel(const Params<T> p)
+{
+    constexpr int PPL = 4;  // pointer triples per lane (P <= 128)
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int m = MS ? MS : p.m, n = NS ? NS : p.n, k = KS ? KS : p.k;
+    const int SA = m * k, SB = k * n, SC = m * n;
+    const int RB = (m + MP::RM - 1) / MP::RM, CB = (n + MP::RN - 1) / MP::RN;
+    const int TPM = RB * CB;
+    const int P = p.P, S = p.S;
+    const int stage_elems = P * (SA + SB + (B0 ? 0 : SC));
+    T *stage0 = reinterpret_cast<T *>(smem_raw);
+    uint64_t *bars = reinterpret_cast<uint64_t *>(stage0 + (long long)S * stage_elems);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int G = gridDim.x;
+    const int my_tiles = (p.ntiles - (int)blockIdx.x + G - 1) / G;
+    const uint64_t pol = policy_evict_first();
+    if (tid == 0) {
+        for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    grid_dep_wait();
+    grid_dep_launch();
+
+    const T *pa[PPL], *pb[PPL];
+    const T *pc[PPL];
+    auto load_ptrs = [&](int i) {  // warp 0: pointers of local tile i
+        const long long pair0 = (blockIdx.x + (long long)i * G) * P;
+#pragma unroll
+        for (int r = 0; r < PPL; ++r) {
+            const long long q = pair0 + lane + 32 * r;
+            const bool ok = i < my_tiles && lane + 32 * r < P && q < p.batch;
+            pa[r] = ok ? p.Ap[q] : nullptr;
+            pb[r] = ok ? p.Bp[q] : nullptr;
+            pc[r] = (ok && !B0) ? (const T *)p.Cp[q] : nullptr;
+        }
+    };
+    auto issue = [&](int i) {  // warp 0: copies of local tile i into stage i % S
+        T *st = stage0 + (long long)(i % S) * stage_elems;
+        uint64_t *bar = &bars[i % S];
+        const uint32_t ba = SA * (uint32_t)sizeof(T), bb = SB * (uint32_t)sizeof(T),
+                       bc = SC * (uint32_t)sizeof(T);
+        uint32_t mine = 0;
+#pragma unroll
+        for (int r = 0; r < PPL; ++r) {
+            if (pa[r] && (((uintptr_t)pa[r] & 15) == 0)) mine += ba;
+            if (pb[r] && (((uintptr_t)pb[r] & 15) == 0)) mine += bb;
+            if (!B0 && pc[r] && (((uintptr_t)pc[r] & 15) == 0)) mine += bc;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
+        if (lane == 0) mbar_arrive_expect_tx(bar, mine);
+        __syncwarp();
+#pragma unroll
+        for (int r = 0; r < PPL; ++r) {
+            const int q = lane + 32 * r;
+            auto copy = [&](T *dst, const T *src, uint32_t bytes, int elems) {
+                if (!src) return;
+                if (((uintptr_t)src & 15) == 0) {
+                    bulk_g2s(dst, src, bytes, bar, pol);
+                } else {
+                    for (int e = 0; e < elems; ++e) dst[e] = src[e];
+                }
+            };
+            copy(st + q * SA, pa[r], ba, SA);
+            copy(st + P * SA + q * SB, pb[r], bb, SB);
+            if (!B0) copy(st + P * (SA + SB) + q * SC, pc[r], bc, SC);
+        }
+    };
+
+    if (warp == 0) {
+        for (int i = 0; i < S - 1 && i < my_tiles; ++i) {
+            load_ptrs(i);
+            issue(i);
+        }
+        load_ptrs(S - 1);
+    }
+    for (int i = 0; i < my_tiles; ++i) {
+        if (warp == 0 && i + S - 1 < my_tiles) {
+            issue(i + S - 1);
+            load_ptrs(i + S);  // consumed next iteration; latency overlaps this tile's compute
+        }
+        const long long pair0 = (blockIdx.x + (long long)i * G) * P;
+        const int np = (int)min((long long)P, p.batch - pair0);
+        const T *st = stage0 + (long long)(i % S) * stage_elems;
+        const T *sA = st, *sB = st + P * SA, *sC = st + P * (SA + SB);
+        mbar_wait(&bars[i % S], (i / S) & 1);
+        const int items = np * TPM;
+        for (int w = tid; w < items; w += NT) {
+            const int q = w / TPM;
+            int rb, cb;
+            split_item<MP>(w - q * TPM, RB, CB, rb, cb);
+            micro_tile<T, MS, NS, KS, OPA, OPB, B0, MP>(sA + q * SA, sB + q * SB,
+                                                        B0 ? nullptr : sC + q * SC,
+                                                        p.Cp[pair0 + q], p.ldc, rb, cb, q, m, n,
+                                                        k, p.alpha, p.beta);
+        }
+        __syncthreads();
+    }
+}
+
+// --------------------------------------------------------------------------
 // General strided / pointer-array batches: element-granular cp.async gathers
 // into a GS-stage ring (packed stage layout identical to the bulk kernel's), C
 // written from registers at its true address.
 // --------------------------------------------------------------------------
 constexpr int GS = 3;
 
-template <class T, int OPA, int OPB, bool B0, class MP, int NT, bool PTR>
+template <class T, int MS, int NS, int KS, int OPA, int OPB, bool B0, class MP, int NT, bool PTR>
 __global__ void __launch_bounds__(NT) gather_kernel(const Params<T> p)
 {
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    const int m = p.m, n = p.n, k = p.k;
+    const int m = MS ? MS : p.m, n = NS ? NS : p.n, k = KS ? KS : p.k;
     const int SA = m * k, SB = k * n, SC = m * n;
     const int rowsA = (OPA == OP_N) ? m : k;
     const int rowsB = (OPB == OP_N) ? k : n;
@@ -419,7 +533,7 @@ __global__ void __launch_bounds__(NT) gather_kernel(const Params<T> p)
             int rb, cb;
             split_item<MP>(w - q * TPM, RB, CB, rb, cb);
             T *cout = PTR ? p.Cp[pair0 + q] : p.C + (pair0 + q) * p.ldc2;
-            micro_tile<T, 0, 0, 0, OPA, OPB, B0, MP>(sA + q * SA, sB + q * SB,
+            micro_tile<T, MS, NS, KS, OPA, OPB, B0, MP>(sA + q * SA, sB + q * SB,
                                                      B0 ? nullptr : sC + q * SC, cout, p.ldc, rb,
                                                      cb, q, m, n, k, p.alpha, p.beta);
         }

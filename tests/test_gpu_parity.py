@@ -245,3 +245,37 @@ def test_tensor_api_matches_torch_layout():
     ref = run_oracle(kind, "N", "N", m, n, k, 0.5, 0.25, A, B, C)
     got = Ct.transpose(1, 2).contiguous().view(-1).cpu().numpy()
     check(kind, "N", "N", m, n, k, 0.5, 0.25, A, B, C, got, ref)
+
+
+# ---------------------------------------------- runtime specialisation (NVRTC)
+@pytest.mark.parametrize("kind", "sdcz")
+def test_jit_instances_match_aot_generic_bitwise(kind):
+    """Non-square packed (bulk), padded (gather) and pointer-array calls run
+    runtime-specialised sm_100a instances; with JIT disabled the generic-size AOT
+    kernels run instead.  Both accumulate in ascending l: results are bitwise equal,
+    and both match the oracle."""
+    import torch
+    from paper_1304_7053_b200 import binding
+
+    if binding.jit_compiled() < 0:
+        pytest.skip("NVRTC unavailable")
+    cases = [((8, 16, 4), (0, 0), "N", "T"), ((5, 7, 3), (2, 3), "T", "N"),
+             ((16, 3, 16), (0, 0), "T", "T")]
+    for (m, n, k), pad, ta, tb in cases:
+        if kind in "cz":
+            tb = tb.replace("T", "C")
+        A, B, C = random_case(kind, m, n, k, 613, ta, tb, seed=31, tag="jit", pad=pad)
+        alpha, beta = _ab(kind, "jit")
+        outs = []
+        for jit in (True, False):
+            prev = binding.set_jit(jit)
+            try:
+                rc, got, path = run_lib(kind, ta, tb, m, n, k, alpha, beta, A, B, C)
+                used_jit = binding.last_path_jit()
+            finally:
+                binding.set_jit(prev)
+            assert rc == 0 and used_jit == jit, (path, used_jit)
+            outs.append(got)
+        assert np.array_equal(outs[0].view(np.uint8), outs[1].view(np.uint8))
+        ref = run_oracle(kind, ta, tb, m, n, k, alpha, beta, A, B, C)
+        check(kind, ta, tb, m, n, k, alpha, beta, A, B, C, outs[0], ref)

@@ -46,9 +46,10 @@ def run_case(kind, m, n, k, batch, ta, tb, general, reps, peak, layout="strided"
             psets.append((A.data_ptr() + perm * (m * k * e), B.data_ptr() + perm * (k * n * e),
                           C.data_ptr() + perm * (m * n * e)))
 
-    def call(s):
+    def call(i):
+        s = sets[i]
         if ptr:
-            pa, pb, pc = psets[sets.index(s)]
+            pa, pb, pc = psets[i]
             rc = tx.tx_gemm_batched_ptr(kind, ta, tb, m, n, k, alpha, pa, lda, pb, ldb, beta, pc,
                                         m, batch)
         else:
@@ -58,12 +59,12 @@ def run_case(kind, m, n, k, batch, ta, tb, general, reps, peak, layout="strided"
         assert rc == 0, tx.status_string(rc)
 
     for i in range(2 * R):
-        call(sets[i % R])
+        call(i % R)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for i in range(reps):
-        call(sets[i % R])
+        call(i % R)
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / reps
