@@ -6,6 +6,7 @@
 // (packed, aligned; size-specialised when m == n == k) [+ gather tail] | gather
 // kernel (any other strided layout) ; tx_gemm_batched_ptr_<t> -> gather kernel
 // over the pointer arrays.
+#include <algorithm>
 #include <atomic>
 #include <cstdint>
 #include <cstdio>
@@ -331,7 +332,11 @@ static int gemm_ptr(char ta, char tb, int m, int n, int k, const U *alpha, const
         // packed matrices whose byte sizes are multiples of 16: per-matrix bulk copies
         const bool bulk_ok = lda == rowsA && ldb == rowsB && ldc == m && (m * k * es) % 16 == 0 &&
                              (k * n * es) % 16 == 0 && (m * n * es) % 16 == 0;
-        e = launch_jit<T>(bulk_ok ? JIT_BULK_PTR : JIT_GATHER_PTR, p, opa, opb, b0, st);
+        // small matrices: 16-byte cp.async chunks over all threads (a per-matrix
+        // TMA copy costs ~80 cycles of issue); >= 512-byte matrices: TMA per matrix
+        const int min_bytes = es * std::min(m * k, std::min(k * n, m * n));
+        const JitKind kind = !bulk_ok ? JIT_GATHER_PTR : (min_bytes >= 512 ? JIT_BULK_PTR : JIT_GATHER_PTR16);
+        e = launch_jit<T>(kind, p, opa, opb, b0, st);
         t_last_path = PATH_PTR | (e == cudaSuccess ? PATH_JIT : 0);
         if (e == cudaErrorNotSupported) e = tab.gather[opa][opb][b0][1](&p, st);
     }

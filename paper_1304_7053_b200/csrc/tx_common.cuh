@@ -190,6 +190,12 @@ __device__ __forceinline__ void cp_async(void *sdst, const void *gsrc)
                  "n"(BYTES)
                  : "memory");
 }
+// 16-byte async copy that bypasses L1 (streamed data).
+__device__ __forceinline__ void cp_async16_cg(void *sdst, const void *gsrc)
+{
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(sdst)), "l"(gsrc)
+                 : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait()

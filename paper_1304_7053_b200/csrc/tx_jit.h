@@ -28,7 +28,8 @@ template <> inline const char *type_name<double>() { return "double"; }
 template <> inline const char *type_name<float2>() { return "float2"; }
 template <> inline const char *type_name<double2>() { return "double2"; }
 
-enum JitKind { JIT_BULK = 0, JIT_BULK_PTR = 1, JIT_GATHER = 2, JIT_GATHER_PTR = 3 };
+enum JitKind { JIT_BULK = 0, JIT_BULK_PTR = 1, JIT_GATHER = 2, JIT_GATHER_PTR = 3,
+               JIT_GATHER_PTR16 = 4 };
 
 // Launch the runtime-specialised kernel of `kind` for p (sizes static in the
 // instance).  Returns cudaErrorNotSupported when JIT is unavailable so the
@@ -38,7 +39,7 @@ cudaError_t launch_jit(JitKind kind, Params<T> p, int opa, int opb, bool b0, cud
 {
     if (!jit_available()) return cudaErrorNotSupported;
     const bool cplx = is_cplx<T>::value;
-    const bool gather = kind == JIT_GATHER || kind == JIT_GATHER_PTR;
+    const bool gather = kind == JIT_GATHER || kind == JIT_GATHER_PTR || kind == JIT_GATHER_PTR16;
     JitMap mp = jit_mapping((int)sizeof(T), cplx, p.m, p.n, p.k, opa, opb,
                             kind != JIT_BULK);
     constexpr int NT = NT_DEFAULT;
@@ -48,7 +49,7 @@ cudaError_t launch_jit(JitKind kind, Params<T> p, int opa, int opb, bool b0, cud
     snprintf(head, sizeof(head), "&tx::%s<%s, %d, %d, %d, %d, %d, %s, ", kname, type_name<T>(),
              p.m, p.n, p.k, opa, opb, b0 ? "true" : "false");
     std::string expr = std::string(head) + jit_map_string(mp) + ", " + std::to_string(NT);
-    if (gather) expr += kind == JIT_GATHER_PTR ? ", true" : ", false";
+    if (gather) expr += kind == JIT_GATHER ? ", false" : (kind == JIT_GATHER_PTR16 ? ", true, true" : ", true");
     expr += ">";
     CUfunction f = jit_function(expr);
     if (!f) return cudaErrorNotSupported;

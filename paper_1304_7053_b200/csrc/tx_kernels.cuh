@@ -467,7 +467,11 @@ __global__ void __launch_bounds__(NT) bulk_ptr_kernel(const Params<T> p)
 // --------------------------------------------------------------------------
 constexpr int GS = 3;
 
-template <class T, int MS, int NS, int KS, int OPA, int OPB, bool B0, class MP, int NT, bool PTR>
+// V16: matrices are packed (ld = rows) with byte sizes that are multiples of 16;
+// they are moved in 16-byte chunks (a chunk whose source is not 16-byte aligned
+// falls back to element copies).
+template <class T, int MS, int NS, int KS, int OPA, int OPB, bool B0, class MP, int NT, bool PTR,
+          bool V16 = false>
 __global__ void __launch_bounds__(NT) gather_kernel(const Params<T> p)
 {
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -482,10 +486,33 @@ __global__ void __launch_bounds__(NT) gather_kernel(const Params<T> p)
     const int G = gridDim.x;
     const int my_tiles = (p.ntiles - (int)blockIdx.x + G - 1) / G;
 
+    auto chunks16 = [&](T *dst0, int elems, int np, long long pair0, const T *const *arr,
+                        const T *base, long long ld2) {
+        const int ch = elems * (int)sizeof(T) / 16;  // chunks per matrix
+        for (int e = tid; e < np * ch; e += NT) {
+            const int q = e / ch, c = e - q * ch;
+            const char *src = reinterpret_cast<const char *>(PTR ? arr[pair0 + q]
+                                                                 : base + (pair0 + q) * ld2) +
+                              16 * c;
+            char *dst = reinterpret_cast<char *>(dst0 + (long long)q * elems) + 16 * c;
+            if ((reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+                cp_async16_cg(dst, src);
+            } else {
+#pragma unroll
+                for (int b = 0; b < 16; b += (int)sizeof(T)) cp_async<sizeof(T)>(dst + b, src + b);
+            }
+        }
+    };
     auto issue = [&](int i) {
         const long long pair0 = (blockIdx.x + (long long)i * G) * P;
         const int np = (int)min((long long)P, p.batch - pair0);
         T *st = stage0 + (long long)(i % GS) * stage_elems;
+        if constexpr (V16) {
+            chunks16(st, SA, np, pair0, p.Ap, p.A, p.lda2);
+            chunks16(st + P * SA, SB, np, pair0, p.Bp, p.B, p.ldb2);
+            if (!B0) chunks16(st + P * (SA + SB), SC, np, pair0, (const T *const *)p.Cp, p.C, p.ldc2);
+            return;
+        }
         for (int e = tid; e < np * SA; e += NT) {
             const int q = e / SA, r = e - q * SA;
             const int row = r % rowsA, col = r / rowsA;
