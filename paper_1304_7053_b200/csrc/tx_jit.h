@@ -55,6 +55,8 @@ cudaError_t launch_jit(JitKind kind, Params<T> p, int opa, int opb, bool b0, cud
     if (!f) return cudaErrorNotSupported;
     Plan pl = plan_tiles(sizeof(T), p.m, p.n, p.k, b0, mp.RM, mp.RN, NT, p.batch, !gather,
                          gather ? GS : mp.S, mp.KB);
+    if (kind == JIT_GATHER_PTR || kind == JIT_GATHER_PTR16)
+        gather_ptr_plan(pl, (int)sizeof(T), p.m, p.n, p.k, b0, p.batch);
     if (kind == JIT_BULK_PTR && pl.P > 128) {  // bulk_ptr_kernel: <= 4 pointer triples per lane
         pl.P = 128;
         pl.ntiles = (int)(((long long)p.batch + 127) / 128);

@@ -470,10 +470,16 @@ constexpr int GS = 3;
 // V16: matrices are packed (ld = rows) with byte sizes that are multiples of 16;
 // they are moved in 16-byte chunks (a chunk whose source is not 16-byte aligned
 // falls back to element copies).
+// PTR: the tile's matrix pointers are staged in shared memory (GS slots of
+// 3 x P pointers, slot = tile % GS).  Each thread loads the pointers of tile
+// i+GS+1 into registers at the end of iteration i and stores them one full
+// iteration later, so the dependent pointer loads never stall a copy issue.
+// The host caps P at 128 (3 x P <= 4 x NT pointer registers).
 template <class T, int MS, int NS, int KS, int OPA, int OPB, bool B0, class MP, int NT, bool PTR,
           bool V16 = false>
 __global__ void __launch_bounds__(NT) gather_kernel(const Params<T> p)
 {
+    constexpr int PR = 4;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int m = MS ? MS : p.m, n = NS ? NS : p.n, k = KS ? KS : p.k;
     const int SA = m * k, SB = k * n, SC = m * n;
@@ -482,18 +488,46 @@ __global__ void __launch_bounds__(NT) gather_kernel(const Params<T> p)
     const int P = p.P;
     const int stage_elems = P * (SA + SB + (B0 ? 0 : SC));
     T *stage0 = reinterpret_cast<T *>(smem_raw);
+    const T **ptab = reinterpret_cast<const T **>(
+        smem_raw + (((long long)GS * stage_elems * sizeof(T) + 15) & ~15ll));
     const int tid = threadIdx.x;
     const int G = gridDim.x;
     const int my_tiles = (p.ntiles - (int)blockIdx.x + G - 1) / G;
 
-    auto chunks16 = [&](T *dst0, int elems, int np, long long pair0, const T *const *arr,
+    // ---- pointer staging (PTR)
+    const T *preg[PR];
+    auto load_regs = [&](int j) {
+        const long long pair0 = (blockIdx.x + (long long)j * G) * P;
+#pragma unroll
+        for (int t = 0; t < PR; ++t) {
+            const int idx = tid + t * NT;
+            const int which = idx / P, q = idx - which * P;
+            const bool ok = PTR && j < my_tiles && which < 3 && pair0 + q < p.batch;
+            const T *const *arr = which == 0 ? p.Ap : (which == 1 ? p.Bp : (const T *const *)p.Cp);
+            preg[t] = ok ? arr[pair0 + q] : nullptr;
+        }
+    };
+    auto store_regs = [&](int j) {
+        const int slot = j % GS;
+#pragma unroll
+        for (int t = 0; t < PR; ++t) {
+            const int idx = tid + t * NT;
+            if (idx < 3 * P) ptab[slot * 3 * P + idx] = preg[t];
+        }
+    };
+    auto ptr_of = [&](int tile, int which, int q, const T *base, long long ld2,
+                      long long pair0) -> const T * {
+        if constexpr (PTR) return ptab[(tile % GS) * 3 * P + which * P + q];
+        else return base + (pair0 + q) * ld2;
+    };
+
+    auto chunks16 = [&](int tile, int which, T *dst0, int elems, int np, long long pair0,
                         const T *base, long long ld2) {
         const int ch = elems * (int)sizeof(T) / 16;  // chunks per matrix
         for (int e = tid; e < np * ch; e += NT) {
             const int q = e / ch, c = e - q * ch;
-            const char *src = reinterpret_cast<const char *>(PTR ? arr[pair0 + q]
-                                                                 : base + (pair0 + q) * ld2) +
-                              16 * c;
+            const char *src =
+                reinterpret_cast<const char *>(ptr_of(tile, which, q, base, ld2, pair0)) + 16 * c;
             char *dst = reinterpret_cast<char *>(dst0 + (long long)q * elems) + 16 * c;
             if ((reinterpret_cast<uintptr_t>(src) & 15) == 0) {
                 cp_async16_cg(dst, src);
@@ -503,42 +537,40 @@ __global__ void __launch_bounds__(NT) gather_kernel(const Params<T> p)
             }
         }
     };
+    auto elems = [&](int tile, int which, T *dst0, int se, int rows, int ld, int np,
+                     long long pair0, const T *base, long long ld2) {
+        for (int e = tid; e < np * se; e += NT) {
+            const int q = e / se, r = e - q * se;
+            const int row = r % rows, col = r / rows;
+            const T *src = ptr_of(tile, which, q, base, ld2, pair0);
+            cp_async<sizeof(T)>(dst0 + e, src + row + (long long)ld * col);
+        }
+    };
     auto issue = [&](int i) {
         const long long pair0 = (blockIdx.x + (long long)i * G) * P;
         const int np = (int)min((long long)P, p.batch - pair0);
         T *st = stage0 + (long long)(i % GS) * stage_elems;
         if constexpr (V16) {
-            chunks16(st, SA, np, pair0, p.Ap, p.A, p.lda2);
-            chunks16(st + P * SA, SB, np, pair0, p.Bp, p.B, p.ldb2);
-            if (!B0) chunks16(st + P * (SA + SB), SC, np, pair0, (const T *const *)p.Cp, p.C, p.ldc2);
-            return;
-        }
-        for (int e = tid; e < np * SA; e += NT) {
-            const int q = e / SA, r = e - q * SA;
-            const int row = r % rowsA, col = r / rowsA;
-            const T *src = PTR ? p.Ap[pair0 + q] : p.A + (pair0 + q) * p.lda2;
-            cp_async<sizeof(T)>(st + e, src + row + (long long)p.lda * col);
-        }
-        T *sb = st + P * SA;
-        for (int e = tid; e < np * SB; e += NT) {
-            const int q = e / SB, r = e - q * SB;
-            const int row = r % rowsB, col = r / rowsB;
-            const T *src = PTR ? p.Bp[pair0 + q] : p.B + (pair0 + q) * p.ldb2;
-            cp_async<sizeof(T)>(sb + e, src + row + (long long)p.ldb * col);
-        }
-        if (!B0) {
-            T *sc = st + P * (SA + SB);
-            for (int e = tid; e < np * SC; e += NT) {
-                const int q = e / SC, r = e - q * SC;
-                const int row = r % m, col = r / m;
-                const T *src = PTR ? p.Cp[pair0 + q] : p.C + (pair0 + q) * p.ldc2;
-                cp_async<sizeof(T)>(sc + e, src + row + (long long)p.ldc * col);
-            }
+            chunks16(i, 0, st, SA, np, pair0, p.A, p.lda2);
+            chunks16(i, 1, st + P * SA, SB, np, pair0, p.B, p.ldb2);
+            if (!B0) chunks16(i, 2, st + P * (SA + SB), SC, np, pair0, p.C, p.ldc2);
+        } else {
+            elems(i, 0, st, SA, rowsA, p.lda, np, pair0, p.A, p.lda2);
+            elems(i, 1, st + P * SA, SB, rowsB, p.ldb, np, pair0, p.B, p.ldb2);
+            if (!B0) elems(i, 2, st + P * (SA + SB), SC, m, p.ldc, np, pair0, p.C, p.ldc2);
         }
     };
 
     grid_dep_wait();
     grid_dep_launch();
+    if constexpr (PTR) {
+        for (int j = 0; j < GS; ++j) {
+            load_regs(j);
+            store_regs(j);
+        }
+        load_regs(GS);
+        __syncthreads();
+    }
     for (int i = 0; i < GS - 1; ++i) {
         if (i < my_tiles) issue(i);
         cp_async_commit();
@@ -559,12 +591,18 @@ __global__ void __launch_bounds__(NT) gather_kernel(const Params<T> p)
             const int q = w / TPM;
             int rb, cb;
             split_item<MP>(w - q * TPM, RB, CB, rb, cb);
-            T *cout = PTR ? p.Cp[pair0 + q] : p.C + (pair0 + q) * p.ldc2;
+            T *cout = PTR ? const_cast<T *>(ptab[(i % GS) * 3 * P + 2 * P + q])
+                          : p.C + (pair0 + q) * p.ldc2;
             micro_tile<T, MS, NS, KS, OPA, OPB, B0, MP>(sA + q * SA, sB + q * SB,
                                                      B0 ? nullptr : sC + q * SC, cout, p.ldc, rb,
                                                      cb, q, m, n, k, p.alpha, p.beta);
         }
         __syncthreads();
+        if constexpr (PTR) {  // slot i % GS is free: pointers of tile i + GS
+            store_regs(i + GS);
+            load_regs(i + GS + 1);
+            __syncthreads();
+        }
     }
     cp_async_wait<0>();
 }
