@@ -241,6 +241,45 @@ static int gemm_strided(char ta, char tb, int m, int n, int k, const U *alpha, c
                         (one || (lda2 == SA && ldb2 == SB && ldc2 == SC)) && aligned16(A) &&
                         aligned16(B) && aligned16(C);
     int path = PATH_GATHER, launches = 0;
+    // fixed-operand batches (the paper's §9 variant): A and/or B shared by every pair
+    const bool bcA = !one && lda2 == 0 && lda == rowsA;
+    const bool bcB = !one && ldb2 == 0 && ldb == rowsB;
+    const bool okA = bcA || (lda == rowsA && (one || lda2 == SA) && aligned16(A));
+    const bool okB = bcB || (ldb == rowsB && (one || ldb2 == SB) && aligned16(B));
+    const bool okC = ldc == m && (one || ldc2 == SC) && aligned16(C);
+    if (!packed && (bcA || bcB) && okA && okB && okC && jit_available()) {
+        const int es = (int)sizeof(U);
+        const int bcast = (bcA ? 1 : 0) | (bcB ? 2 : 0);
+        int g = (int)(SC * es);
+        if (!bcA) g = gcd_i(g, (int)(SA * es));
+        if (!bcB) g = gcd_i(g, (int)(SB * es));
+        const int unit = 16 / gcd_i(16, g);
+        const int main_pairs = batch / unit * unit;
+        if (main_pairs > 0) {
+            Params<T> q = p;
+            q.batch = main_pairs;
+            const cudaError_t e = launch_jit<T>(JIT_BULK, q, opa, opb, b0, st, bcast);
+            if (e != cudaSuccess && e != cudaErrorNotSupported) return as_status(e);
+            if (e == cudaSuccess) {
+                ++launches;
+                path = PATH_BULK | PATH_JIT;
+                if (main_pairs < batch) {
+                    Params<T> r = p;
+                    r.batch = batch - main_pairs;
+                    if (!bcA) r.A += lda2 * main_pairs;
+                    if (!bcB) r.B += ldb2 * main_pairs;
+                    r.C += ldc2 * main_pairs;
+                    const cudaError_t e2 = tab.gather[opa][opb][b0][0](&r, st);
+                    if (e2 != cudaSuccess) return as_status(e2);
+                    ++launches;
+                    path |= PATH_TAIL;
+                }
+                t_last_path = path;
+                t_last_launches = launches;
+                return 0;
+            }
+        }
+    }
     if (packed) {
         const int es = (int)sizeof(U);
         const int unit = 16 / gcd_i(16, gcd_i((int)(SA * es), gcd_i((int)(SB * es), (int)(SC * es))));

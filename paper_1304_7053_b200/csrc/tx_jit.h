@@ -35,7 +35,8 @@ enum JitKind { JIT_BULK = 0, JIT_BULK_PTR = 1, JIT_GATHER = 2, JIT_GATHER_PTR = 
 // instance).  Returns cudaErrorNotSupported when JIT is unavailable so the
 // caller can use an AOT kernel instead.
 template <class T>
-cudaError_t launch_jit(JitKind kind, Params<T> p, int opa, int opb, bool b0, cudaStream_t st)
+cudaError_t launch_jit(JitKind kind, Params<T> p, int opa, int opb, bool b0, cudaStream_t st,
+                       int bcast = 0)
 {
     if (!jit_available()) return cudaErrorNotSupported;
     const bool cplx = is_cplx<T>::value;
@@ -50,11 +51,12 @@ cudaError_t launch_jit(JitKind kind, Params<T> p, int opa, int opb, bool b0, cud
              p.m, p.n, p.k, opa, opb, b0 ? "true" : "false");
     std::string expr = std::string(head) + jit_map_string(mp) + ", " + std::to_string(NT);
     if (gather) expr += kind == JIT_GATHER ? ", false" : (kind == JIT_GATHER_PTR16 ? ", true, true" : ", true");
+    if (kind == JIT_BULK && bcast) expr += ", " + std::to_string(bcast);
     expr += ">";
     CUfunction f = jit_function(expr);
     if (!f) return cudaErrorNotSupported;
     Plan pl = plan_tiles(sizeof(T), p.m, p.n, p.k, b0, mp.RM, mp.RN, NT, p.batch, !gather,
-                         gather ? GS : mp.S, mp.KB);
+                         gather ? GS : mp.S, mp.KB, kind == JIT_BULK ? bcast : 0);
     if (kind == JIT_GATHER_PTR || kind == JIT_GATHER_PTR16)
         gather_ptr_plan(pl, (int)sizeof(T), p.m, p.n, p.k, b0, p.batch);
     if (kind == JIT_BULK_PTR && pl.P > 128) {  // bulk_ptr_kernel: <= 4 pointer triples per lane

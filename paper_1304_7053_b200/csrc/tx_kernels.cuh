@@ -284,18 +284,28 @@ __device__ __forceinline__ void split_item(int sub, int RB, int CB, int &rb, int
 // C^p is stored from registers straight to global memory (vectorised along the
 // contiguous rows by the mapping), so no output staging is needed.
 // --------------------------------------------------------------------------
-template <class T, int MS, int NS, int KS, int OPA, int OPB, bool B0, class MP, int NT>
+// BCAST (fixed-operand batched GEMM, the paper's §9 variant):
+// bit 0 = A is one matrix shared by every pair (lda2 = 0), bit 1 = same for B.
+// A shared operand is loaded once per CTA into its own shared-memory region and
+// is not part of the streamed stages, so a pair moves 2 matrices instead of 3.
+template <class T, int MS, int NS, int KS, int OPA, int OPB, bool B0, class MP, int NT,
+          int BCAST = 0>
 __global__ void __launch_bounds__(NT) bulk_kernel(const Params<T> p)
 {
+    constexpr bool BA = (BCAST & 1) != 0, BB = (BCAST & 2) != 0;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int m = MS ? MS : p.m, n = NS ? NS : p.n, k = KS ? KS : p.k;
     const int SA = m * k, SB = k * n, SC = m * n;
+    const int sSA = BA ? 0 : SA, sSB = BB ? 0 : SB;  // per-pair elements in a stage
     const int RB = (m + MP::RM - 1) / MP::RM, CB = (n + MP::RN - 1) / MP::RN;
     const int TPM = RB * CB;
     const int P = p.P, S = p.S;
-    const int stage_elems = P * (SA + SB + (B0 ? 0 : SC));
+    const int stage_elems = P * (sSA + sSB + (B0 ? 0 : SC));
     T *stage0 = reinterpret_cast<T *>(smem_raw);
-    uint64_t *bars = reinterpret_cast<uint64_t *>(stage0 + (long long)S * stage_elems);
+    T *shared_ab = stage0 + (long long)S * stage_elems;  // broadcast A then B (packed)
+    uint64_t *bars = reinterpret_cast<uint64_t *>(
+        smem_raw + (((long long)S * stage_elems + (BA ? SA : 0) + (BB ? SB : 0)) * sizeof(T) + 15) /
+                       16 * 16);
 
     const int tid = threadIdx.x;
     const int G = gridDim.x;
@@ -309,19 +319,26 @@ __global__ void __launch_bounds__(NT) bulk_kernel(const Params<T> p)
     __syncthreads();
     grid_dep_wait();    // PDL: the prologue above overlapped the previous grid's tail
     grid_dep_launch();
+    if constexpr (BA || BB) {  // the shared operand(s), once per CTA (any alignment)
+        if (BA)
+            for (int e = threadIdx.x; e < SA; e += NT) shared_ab[e] = p.A[e];
+        if (BB)
+            for (int e = threadIdx.x; e < SB; e += NT) shared_ab[(BA ? SA : 0) + e] = p.B[e];
+        __syncthreads();
+    }
 
     auto issue = [&](int i) {  // local tile i -> stage i % S (thread 0 only)
         const long long pair0 = (blockIdx.x + (long long)i * G) * P;
         const int np = (int)min((long long)P, p.batch - pair0);
         T *st = stage0 + (long long)(i % S) * stage_elems;
-        const uint32_t ba = np * SA * (uint32_t)sizeof(T);
-        const uint32_t bb = np * SB * (uint32_t)sizeof(T);
+        const uint32_t ba = BA ? 0u : np * SA * (uint32_t)sizeof(T);
+        const uint32_t bb = BB ? 0u : np * SB * (uint32_t)sizeof(T);
         const uint32_t bcin = B0 ? 0u : np * SC * (uint32_t)sizeof(T);
         uint64_t *bar = &bars[i % S];
         mbar_arrive_expect_tx(bar, ba + bb + bcin);
-        bulk_g2s(st, p.A + pair0 * SA, ba, bar, pol);
-        bulk_g2s(st + P * SA, p.B + pair0 * SB, bb, bar, pol);
-        if (!B0) bulk_g2s(st + P * (SA + SB), p.C + pair0 * SC, bcin, bar, pol);
+        if (!BA) bulk_g2s(st, p.A + pair0 * SA, ba, bar, pol);
+        if (!BB) bulk_g2s(st + P * sSA, p.B + pair0 * SB, bb, bar, pol);
+        if (!B0) bulk_g2s(st + P * (sSA + sSB), p.C + pair0 * SC, bcin, bar, pol);
     };
 
     if (tid == 0)
@@ -332,7 +349,9 @@ __global__ void __launch_bounds__(NT) bulk_kernel(const Params<T> p)
         const long long pair0 = (blockIdx.x + (long long)i * G) * P;
         const int np = (int)min((long long)P, p.batch - pair0);
         const T *st = stage0 + (long long)(i % S) * stage_elems;
-        const T *sA = st, *sB = st + P * SA, *sC = st + P * (SA + SB);
+        const T *sA = BA ? shared_ab : st;
+        const T *sB = BB ? shared_ab + (BA ? SA : 0) : st + P * sSA;
+        const T *sC = st + P * (sSA + sSB);
         T *gC = p.C + pair0 * SC;
         mbar_wait(&bars[i % S], (i / S) & 1);
         const int items = np * TPM;
@@ -340,7 +359,8 @@ __global__ void __launch_bounds__(NT) bulk_kernel(const Params<T> p)
             const int q = w / TPM;
             int rb, cb;
             split_item<MP>(w - q * TPM, RB, CB, rb, cb);
-            micro_tile<T, MS, NS, KS, OPA, OPB, B0, MP>(sA + q * SA, sB + q * SB,
+            micro_tile<T, MS, NS, KS, OPA, OPB, B0, MP>(sA + (BA ? 0 : q * SA),
+                                                        sB + (BB ? 0 : q * SB),
                                                         B0 ? nullptr : sC + q * SC, gC + q * SC,
                                                         m, rb, cb, q, m, n, k, p.alpha, p.beta);
         }

@@ -20,13 +20,19 @@ def flops(kind: str, m: int, n: int, k: int, batch: int) -> int:
 
 
 def bytes_moved(kind: str, m: int, n: int, k: int, batch: int, alpha_nonzero: bool = True,
-                beta_nonzero: bool = False, pointer_arrays: bool = False) -> int:
+                beta_nonzero: bool = False, pointer_arrays: bool = False,
+                shared_a: bool = False, shared_b: bool = False) -> int:
+    """shared_a / shared_b: fixed-operand batch (ld2 = 0), the shared
+    matrix is read once for the whole batch."""
     s = ESIZE[kind]
     reads_ab = alpha_nonzero and k > 0
-    per = s * ((m * k + k * n if reads_ab else 0) + m * n * (2 if beta_nonzero else 1))
+    a = 0 if (shared_a or not reads_ab) else m * k
+    b = 0 if (shared_b or not reads_ab) else k * n
+    per = s * (a + b + m * n * (2 if beta_nonzero else 1))
     if pointer_arrays:
         per += 8 * ((2 if reads_ab else 0) + 1)
-    return per * batch
+    once = s * ((m * k if shared_a and reads_ab else 0) + (k * n if shared_b and reads_ab else 0))
+    return per * batch + (once if batch else 0)
 
 
 def footprint(kind: str, m: int, n: int, k: int, batch: int) -> int:

@@ -141,18 +141,34 @@ def test_misaligned_base_uses_gather(kind):
 
 
 @pytest.mark.parametrize("kind", "sdcz")
-def test_broadcast_A_ld2_zero(kind):
-    """lda2 = 0: one A for every pair (the paper's fixed-operand variant, §9)."""
-    n, batch = 6, 411
-    A, B, C = random_case(kind, n, n, n, batch, seed=10, tag="bc")
-    A1 = Operand(kind, n, n, 1, txinputs.stream_key(10, "bcA"))
-    A1.ld2 = 0
-    A1.batch = batch
-    alpha, beta = _ab(kind, "bc")
-    rc, got, _ = run_lib(kind, "N", "N", n, n, n, alpha, beta, A1, B, C)
-    assert rc == 0
-    ref = run_oracle(kind, "N", "N", n, n, n, alpha, beta, A1, B, C)
-    check(kind, "N", "N", n, n, n, alpha, beta, A1, B, C, got, ref)
+@pytest.mark.parametrize("which", ["A", "B", "AB"])
+def test_fixed_operand_ld2_zero(kind, which):
+    """lda2 = 0 / ldb2 = 0: one A (or B) for every pair -- the paper's fixed-operand
+    variant (§9).  Packed otherwise, it runs the bulk kernel with the
+    shared operand resident in shared memory (runtime-specialised instance)."""
+    from paper_1304_7053_b200 import binding
+
+    for (m, n, k), ta, tb, batch in (((6, 6, 6), "N", "N", 411), ((16, 16, 16), "T", "N", 1000),
+                                     ((8, 16, 4), "N", "T", 777), ((5, 3, 7), "T", "T", 513)):
+        if kind in "cz":
+            ta = ta.replace("T", "C")
+        A, B, C = random_case(kind, m, n, k, batch, ta, tb, seed=10, tag="bc" + which)
+        ra, ca = stored_shape(ta, m, k)
+        rb, cb = stored_shape(tb, k, n)
+        if "A" in which:
+            A = Operand(kind, ra, ca, 1, txinputs.stream_key(10, "bcA", m, n, k))
+            A.ld2, A.batch = 0, batch
+        if "B" in which:
+            B = Operand(kind, rb, cb, 1, txinputs.stream_key(10, "bcB", m, n, k))
+            B.ld2, B.batch = 0, batch
+        for general in (False, True):
+            alpha, beta = _ab(kind, "bc" + which, general)
+            rc, got, path = run_lib(kind, ta, tb, m, n, k, alpha, beta, A, B, C)
+            assert rc == 0
+            if binding.jit_compiled() >= 0:
+                assert path[0] in ("bulk", "bulk+tail"), path
+            ref = run_oracle(kind, ta, tb, m, n, k, alpha, beta, A, B, C)
+            check(kind, ta, tb, m, n, k, alpha, beta, A, B, C, got, ref)
 
 
 @pytest.mark.parametrize("kind", "sdcz")

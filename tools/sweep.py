@@ -25,6 +25,7 @@ def run_case(kind, m, n, k, batch, ta, tb, general, reps, peak, layout="strided"
     es = model.ESIZE[kind]
     per_set = es * (m * k + k * n + m * n) * batch
     ptr = layout == "ptr"
+    shA, shB = layout == "sharedA", layout == "sharedB"
     R = max(1, min(8, -(-4 * L2 // per_set)))
     sets = []
     for r in range(R):
@@ -54,8 +55,8 @@ def run_case(kind, m, n, k, batch, ta, tb, general, reps, peak, layout="strided"
                                         m, batch)
         else:
             A, B, C = s
-            rc = tx.tx_gemm_batched(kind, ta, tb, m, n, k, alpha, A, lda, m * k, B, ldb, k * n,
-                                    beta, C, m, m * n, batch)
+            rc = tx.tx_gemm_batched(kind, ta, tb, m, n, k, alpha, A, lda, 0 if shA else m * k, B,
+                                    ldb, 0 if shB else k * n, beta, C, m, m * n, batch)
         assert rc == 0, tx.status_string(rc)
 
     for i in range(2 * R):
@@ -68,7 +69,7 @@ def run_case(kind, m, n, k, batch, ta, tb, general, reps, peak, layout="strided"
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / reps
-    byts = model.bytes_moved(kind, m, n, k, batch, True, general)
+    byts = model.bytes_moved(kind, m, n, k, batch, True, general, shared_a=shA, shared_b=shB)
     if ptr:
         byts_ptr = model.bytes_moved(kind, m, n, k, batch, True, general, pointer_arrays=True)
     gbps = byts / (ms / 1e3) / 1e9
@@ -89,7 +90,7 @@ def main():
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--out", default="")
     ap.add_argument("--shapes", default="", help="m x n x k list, e.g. 8x16x4,16x3x16")
-    ap.add_argument("--layout", default="strided", choices=("strided", "ptr"))
+    ap.add_argument("--layout", default="strided", choices=("strided", "ptr", "sharedA", "sharedB"))
     a = ap.parse_args()
     lo, hi = (int(x) for x in a.sizes.split("-")) if "-" in a.sizes else (int(a.sizes),) * 2
     peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
