@@ -20,7 +20,7 @@ import subprocess
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libtxgemm.so")
+LIB_PATH = os.environ.get("TXGEMM_LIB") or os.path.join(_HERE, "libtxgemm.so")
 
 KINDS = ("s", "d", "c", "z")
 PATHS = {0: "none", 1: "bulk", 2: "gather", 3: "ptr", 4: "scale", 17: "bulk+tail",
