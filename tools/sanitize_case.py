@@ -1,0 +1,44 @@
+"""Small cases for compute-sanitizer (SURVEY §4 tier T1s).  Exercises the bulk
+(TMA + mbarrier) kernels, the gather / pointer kernels (JIT) and the scale kernel.
+With --uninit-c, C is allocated with cudaMalloc and never written before the
+beta == 0 call: initcheck then proves the beta == 0 path never reads C."""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import torch  # noqa: E402
+
+import paper_1304_7053_b200 as tx  # noqa: E402
+import txinputs  # noqa: E402
+
+
+def main():
+    uninit = "--uninit-c" in sys.argv
+    for kind, n, batch in (("s", 16, 3000), ("d", 5, 1001), ("c", 8, 517), ("z", 3, 999)):
+        e = n * n
+        A = txinputs.values_torch(kind, 1, 0, e * batch, "cuda")
+        B = txinputs.values_torch(kind, 2, 0, e * batch, "cuda")
+        C = torch.empty(e * batch, dtype=A.dtype, device="cuda")  # uninitialised
+        assert tx.tx_gemm_batched(kind, "N", "T", n, n, n, 1.0, A, n, e, B, n, e, 0.0, C, n, e,
+                                  batch) == 0
+        if not uninit:
+            assert tx.tx_gemm_batched(kind, "T", "N", n, n, n, 0.5, A, n, e, B, n, e, 0.25, C, n, e,
+                                      batch) == 0
+            assert tx.tx_gemm_batched(kind, "N", "N", n, n, n, 0.0, A, n, e, B, n, e, 0.5, C, n, e,
+                                      batch) == 0
+            # pointer arrays and a padded layout (gather kernels)
+            es = A.element_size()
+            idx = torch.arange(batch, device="cuda")
+            pa, pb, pc = (X.data_ptr() + idx * (e * es) for X in (A, B, C))
+            assert tx.tx_gemm_batched_ptr(kind, "N", "N", n, n, n, 0.5, pa, n, pb, n, 0.25, pc, n,
+                                          batch) == 0
+            Cp = torch.zeros((e + 3) * batch, dtype=A.dtype, device="cuda")
+            assert tx.tx_gemm_batched(kind, "N", "N", n, n, n, 1.0, A, n, e, B, n, e, 0.5, Cp, n,
+                                      e + 3, batch) == 0
+    torch.cuda.synchronize()
+    print("ok")
+
+
+if __name__ == "__main__":
+    main()
