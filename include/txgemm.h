@@ -35,8 +35,8 @@
  * device memory (the host-buffer entry creates two copy streams per device once,
  * and a few events per call).  A, B, C, the pointer arrays and their targets are device
  * memory of the CURRENT device.  alpha and beta are HOST pointers, read before
- * the call returns (the paper allows host or device; device
- * mode is out of scope, reading R12).
+ * the call returns (the paper allows host or device; the
+ * *_dev entries below take device-resident alpha/beta).
  *
  * Execution.  Asynchronous on `stream` (NULL = legacy default stream); returns
  * after enqueueing.  Reentrant and thread-safe.  Results are bitwise
@@ -144,6 +144,50 @@ int tx_gemm_batched_hostio_z(char transa, char transb, int m, int n, int k,
                              const tx_cdouble *beta, tx_cdouble *hC, int ldc, long long ldc2,
                              int batch_count, tx_stream_t stream, tx_cdouble *dA,
                              tx_cdouble *dB, tx_cdouble *dC);
+
+/* ---- device-resident alpha / beta (the paper's "host or device pointer",
+ * PAPER.md:347, 354): identical to tx_gemm_batched_<t> / tx_gemm_batched_ptr_<t>
+ * except that alpha and beta point to DEVICE memory and are read by the kernels
+ * when they run (stream-ordered), so the call never synchronises.  The kernels
+ * decide at run time: alpha == 0 -> C <- beta*C without reading A and B (nothing
+ * when beta == 1); beta == 0 -> C is never read.  Because the values are not
+ * known at the call, A and B must be valid whenever m*n*batch_count > 0 and
+ * k > 0, and the overlap check of the strided call always applies.  Argument
+ * positions and the other checks are those of the host-scalar calls. ---- */
+int tx_gemm_batched_dev_s(char transa, char transb, int m, int n, int k, const float *alpha,
+                          const float *A, int lda, long long lda2, const float *B, int ldb,
+                          long long ldb2, const float *beta, float *C, int ldc, long long ldc2,
+                          int batch_count, tx_stream_t stream);
+int tx_gemm_batched_dev_d(char transa, char transb, int m, int n, int k, const double *alpha,
+                          const double *A, int lda, long long lda2, const double *B, int ldb,
+                          long long ldb2, const double *beta, double *C, int ldc, long long ldc2,
+                          int batch_count, tx_stream_t stream);
+int tx_gemm_batched_dev_c(char transa, char transb, int m, int n, int k, const tx_cfloat *alpha,
+                          const tx_cfloat *A, int lda, long long lda2, const tx_cfloat *B, int ldb,
+                          long long ldb2, const tx_cfloat *beta, tx_cfloat *C, int ldc,
+                          long long ldc2, int batch_count, tx_stream_t stream);
+int tx_gemm_batched_dev_z(char transa, char transb, int m, int n, int k, const tx_cdouble *alpha,
+                          const tx_cdouble *A, int lda, long long lda2, const tx_cdouble *B,
+                          int ldb, long long ldb2, const tx_cdouble *beta, tx_cdouble *C, int ldc,
+                          long long ldc2, int batch_count, tx_stream_t stream);
+int tx_gemm_batched_ptr_dev_s(char transa, char transb, int m, int n, int k, const float *alpha,
+                              const float *const *Aarray, int lda, const float *const *Barray,
+                              int ldb, const float *beta, float *const *Carray, int ldc,
+                              int batch_count, tx_stream_t stream);
+int tx_gemm_batched_ptr_dev_d(char transa, char transb, int m, int n, int k, const double *alpha,
+                              const double *const *Aarray, int lda, const double *const *Barray,
+                              int ldb, const double *beta, double *const *Carray, int ldc,
+                              int batch_count, tx_stream_t stream);
+int tx_gemm_batched_ptr_dev_c(char transa, char transb, int m, int n, int k,
+                              const tx_cfloat *alpha, const tx_cfloat *const *Aarray, int lda,
+                              const tx_cfloat *const *Barray, int ldb, const tx_cfloat *beta,
+                              tx_cfloat *const *Carray, int ldc, int batch_count,
+                              tx_stream_t stream);
+int tx_gemm_batched_ptr_dev_z(char transa, char transb, int m, int n, int k,
+                              const tx_cdouble *alpha, const tx_cdouble *const *Aarray, int lda,
+                              const tx_cdouble *const *Barray, int ldb, const tx_cdouble *beta,
+                              tx_cdouble *const *Carray, int ldc, int batch_count,
+                              tx_stream_t stream);
 
 /* ---- introspection and tuning (host only, no GPU work) ---- */
 /* Human-readable text for a status code (static storage, never NULL). */

@@ -9,7 +9,8 @@ is its thin binding (binding.py) plus the host-side work model (model.py).
 from . import model  # noqa: F401
 from .binding import (TxError, build, gemm_batched, last_path, lib, num_instances, set_tuning,  # noqa: F401,E501
                       pointer_array, set_max_ctas, status_string, tx_gemm_batched,
-                      tx_gemm_batched_hostio, tx_gemm_batched_ptr, version)
+                      tx_gemm_batched_dev, tx_gemm_batched_hostio, tx_gemm_batched_ptr,
+                      tx_gemm_batched_ptr_dev, version)
 from .binding import (tx_gemm_batched_s, tx_gemm_batched_d, tx_gemm_batched_c,  # noqa: F401
                       tx_gemm_batched_z, tx_gemm_batched_ptr_s, tx_gemm_batched_ptr_d,
                       tx_gemm_batched_ptr_c, tx_gemm_batched_ptr_z, tx_gemm_batched_hostio_s,

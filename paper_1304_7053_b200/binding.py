@@ -77,6 +77,13 @@ def lib():
             h.argtypes = [cc, cc, ci, ci, ci, vp, vp, ci, cll, vp, ci, cll, vp, vp, ci, cll, ci, vp,
                           vp, vp, vp]
             h.restype = ci
+        for k in KINDS:
+            f = getattr(L, f"tx_gemm_batched_dev_{k}")
+            f.argtypes = [cc, cc, ci, ci, ci, vp, vp, ci, cll, vp, ci, cll, vp, vp, ci, cll, ci, vp]
+            f.restype = ci
+            g = getattr(L, f"tx_gemm_batched_ptr_dev_{k}")
+            g.argtypes = [cc, cc, ci, ci, ci, vp, vp, ci, vp, ci, vp, vp, ci, ci, vp]
+            g.restype = ci
         L.tx_status_string.argtypes = [ci]
         L.tx_status_string.restype = ctypes.c_char_p
         L.tx_version.restype = ci
@@ -203,6 +210,21 @@ def tx_gemm_batched_hostio(kind, transa, transb, m, n, k, alpha, hA, lda, lda2, 
         _addr(dA), _addr(dB), _addr(dC))
 
 
+def tx_gemm_batched_dev(kind, transa, transb, m, n, k, alpha_dev, A, lda, lda2, B, ldb, ldb2,
+                        beta_dev, C, ldc, ldc2, batch_count, stream=None):
+    """Strided call with DEVICE-resident alpha / beta (device addresses or 1-element tensors)."""
+    return getattr(lib(), f"tx_gemm_batched_dev_{kind}")(
+        _op(transa), _op(transb), m, n, k, _addr(alpha_dev), _addr(A), lda, lda2, _addr(B), ldb,
+        ldb2, _addr(beta_dev), _addr(C), ldc, ldc2, batch_count, _stream(stream))
+
+
+def tx_gemm_batched_ptr_dev(kind, transa, transb, m, n, k, alpha_dev, Aarray, lda, Barray, ldb,
+                            beta_dev, Carray, ldc, batch_count, stream=None):
+    return getattr(lib(), f"tx_gemm_batched_ptr_dev_{kind}")(
+        _op(transa), _op(transb), m, n, k, _addr(alpha_dev), _addr(Aarray), lda, _addr(Barray),
+        ldb, _addr(beta_dev), _addr(Carray), ldc, batch_count, _stream(stream))
+
+
 def _named(kind, fn):
     def f(*args, **kw):
         return fn(kind, *args, **kw)
@@ -216,6 +238,8 @@ for _k in KINDS:
     globals()[f"tx_gemm_batched_{_k}"] = _named(_k, tx_gemm_batched)
     globals()[f"tx_gemm_batched_ptr_{_k}"] = _named(_k, tx_gemm_batched_ptr)
     globals()[f"tx_gemm_batched_hostio_{_k}"] = _named(_k, tx_gemm_batched_hostio)
+    globals()[f"tx_gemm_batched_dev_{_k}"] = _named(_k, tx_gemm_batched_dev)
+    globals()[f"tx_gemm_batched_ptr_dev_{_k}"] = _named(_k, tx_gemm_batched_ptr_dev)
 
 
 # ------------------------------------------------------------ tensor API

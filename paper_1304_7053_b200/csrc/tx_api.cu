@@ -327,6 +327,153 @@ static int gemm_strided(char ta, char tb, int m, int n, int k, const U *alpha, c
     return 0;
 }
 
+// ------------------------------------------- device-resident alpha / beta
+// The values are only known on the device: the kernels decide alpha == 0 and
+// beta == 0 at run time (R12).  A and B must be valid whenever
+// m*n*batch > 0 and k > 0 (they may be read).
+template <class U>
+static int gemm_strided_dev(char ta, char tb, int m, int n, int k, const U *alpha, const U *A,
+                            int lda, long long lda2, const U *B, int ldb, long long ldb2,
+                            const U *beta, U *C, int ldc, long long ldc2, int batch,
+                            cudaStream_t st)
+{
+    using AT = Api<U>;
+    using T = typename AT::T;
+    const int rc = validate(false, ta, tb, m, n, k, alpha, false, beta, A, lda, lda2, B, ldb,
+                            ldb2, C, ldc, ldc2, batch, sizeof(U));
+    if (rc) return rc;
+    if (m == 0 || n == 0 || batch == 0) {
+        t_last_path = PATH_NONE;
+        t_last_launches = 0;
+        return 0;
+    }
+    TypeTables &tab = tables(AT::id);
+    Params<T> p;
+    std::memset(&p, 0, sizeof(p));
+    p.A = reinterpret_cast<const T *>(A);
+    p.B = reinterpret_cast<const T *>(B);
+    p.C = reinterpret_cast<T *>(C);
+    p.lda = lda;
+    p.ldb = ldb;
+    p.ldc = ldc;
+    p.lda2 = lda2;
+    p.ldb2 = ldb2;
+    p.ldc2 = ldc2;
+    p.m = m;
+    p.n = n;
+    p.k = k;
+    p.batch = batch;
+    p.alpha_dev = reinterpret_cast<const T *>(alpha);
+    p.beta_dev = reinterpret_cast<const T *>(beta);
+    cudaError_t e;
+    if (k == 0) {
+        e = tab.scale_dev[0](&p, st);
+        if (e != cudaSuccess) return as_status(e);
+        t_last_path = PATH_SCALE;
+        t_last_launches = 1;
+        return 0;
+    }
+    const int opa = op_code(ta, AT::cplx), opb = op_code(tb, AT::cplx);
+    const int rowsA = op_n(ta) ? m : k, colsA = op_n(ta) ? k : m;
+    const int rowsB = op_n(tb) ? k : n, colsB = op_n(tb) ? n : k;
+    const long long SA = (long long)rowsA * colsA, SB = (long long)rowsB * colsB,
+                    SC = (long long)m * n;
+    const bool one = batch == 1;
+    const bool packed = lda == rowsA && ldb == rowsB && ldc == m &&
+                        (one || (lda2 == SA && ldb2 == SB && ldc2 == SC)) && aligned16(A) &&
+                        aligned16(B) && aligned16(C);
+    int launches = 0, path = PATH_GATHER;
+    if (packed) {
+        const int es = (int)sizeof(U);
+        const int unit = 16 / gcd_i(16, gcd_i((int)(SA * es), gcd_i((int)(SB * es), (int)(SC * es))));
+        const int main_pairs = batch / unit * unit;
+        if (main_pairs > 0) {
+            Params<T> q = p;
+            q.batch = main_pairs;
+            q.lda2 = SA;
+            q.ldb2 = SB;
+            q.ldc2 = SC;
+            e = launch_jit<T>(JIT_BULK, q, opa, opb, false, st, 0, true);
+            path = PATH_BULK | (e == cudaSuccess ? PATH_JIT : 0);
+            if (e == cudaErrorNotSupported) e = tab.bulk_dyn_dev[opa][opb](&q, st);
+            if (e != cudaSuccess) return as_status(e);
+            ++launches;
+        }
+        if (main_pairs < batch) {
+            Params<T> q = p;
+            q.batch = batch - main_pairs;
+            q.lda2 = SA;
+            q.ldb2 = SB;
+            q.ldc2 = SC;
+            q.A += SA * main_pairs;
+            q.B += SB * main_pairs;
+            q.C += SC * main_pairs;
+            e = tab.gather_dev[opa][opb][0](&q, st);
+            if (e != cudaSuccess) return as_status(e);
+            ++launches;
+            path = main_pairs > 0 ? (path | PATH_TAIL) : PATH_GATHER;
+        }
+    } else {
+        e = launch_jit<T>(JIT_GATHER, p, opa, opb, false, st, 0, true);
+        if (e == cudaSuccess) path |= PATH_JIT;
+        if (e == cudaErrorNotSupported) e = tab.gather_dev[opa][opb][0](&p, st);
+        if (e != cudaSuccess) return as_status(e);
+        launches = 1;
+    }
+    t_last_path = path;
+    t_last_launches = launches;
+    return 0;
+}
+
+template <class U>
+static int gemm_ptr_dev(char ta, char tb, int m, int n, int k, const U *alpha, const U *const *Aa,
+                        int lda, const U *const *Ba, int ldb, const U *beta, U *const *Ca, int ldc,
+                        int batch, cudaStream_t st)
+{
+    using AT = Api<U>;
+    using T = typename AT::T;
+    const int rc = validate(true, ta, tb, m, n, k, alpha, false, beta, Aa, lda, 0, Ba, ldb, 0, Ca,
+                            ldc, 0, batch, sizeof(U));
+    if (rc) return rc;
+    if (m == 0 || n == 0 || batch == 0) {
+        t_last_path = PATH_NONE;
+        t_last_launches = 0;
+        return 0;
+    }
+    TypeTables &tab = tables(AT::id);
+    Params<T> p;
+    std::memset(&p, 0, sizeof(p));
+    p.Ap = reinterpret_cast<const T *const *>(Aa);
+    p.Bp = reinterpret_cast<const T *const *>(Ba);
+    p.Cp = reinterpret_cast<T *const *>(Ca);
+    p.lda = lda;
+    p.ldb = ldb;
+    p.ldc = ldc;
+    p.m = m;
+    p.n = n;
+    p.k = k;
+    p.batch = batch;
+    p.alpha_dev = reinterpret_cast<const T *>(alpha);
+    p.beta_dev = reinterpret_cast<const T *>(beta);
+    cudaError_t e;
+    if (k == 0) {
+        e = tab.scale_dev[1](&p, st);
+        t_last_path = PATH_SCALE;
+    } else {
+        const int opa = op_code(ta, AT::cplx), opb = op_code(tb, AT::cplx);
+        const int rowsA = op_n(ta) ? m : k, rowsB = op_n(tb) ? k : n;
+        const int es = (int)sizeof(U);
+        const bool v16 = lda == rowsA && ldb == rowsB && ldc == m && (m * k * es) % 16 == 0 &&
+                         (k * n * es) % 16 == 0 && (m * n * es) % 16 == 0;
+        e = launch_jit<T>(v16 ? JIT_GATHER_PTR16 : JIT_GATHER_PTR, p, opa, opb, false, st, 0, true);
+        t_last_path = PATH_PTR | (e == cudaSuccess ? PATH_JIT : 0);
+        if (e == cudaErrorNotSupported) e = tab.gather_dev[opa][opb][1](&p, st);
+    }
+    if (e != cudaSuccess) return as_status(e);
+    t_last_launches = 1;
+    return 0;
+}
+
 // -------------------------------------------------------- pointer-array call
 template <class U>
 static int gemm_ptr(char ta, char tb, int m, int n, int k, const U *alpha, const U *const *Aa,
@@ -527,6 +674,30 @@ using namespace tx;
         return gemm_hostio<U>(ta, tb, m, n, k, alpha, hA, lda, lda2, hB, ldb, ldb2, beta, hC,     \
                               ldc, ldc2, batch, (cudaStream_t)stream, dA, dB, dC);                \
     }
+
+#define TX_DEV(SUF, U)                                                                            \
+    extern "C" int tx_gemm_batched_dev_##SUF(char ta, char tb, int m, int n, int k, const U *alpha,\
+                                             const U *A, int lda, long long lda2, const U *B,       \
+                                             int ldb, long long ldb2, const U *beta, U *C, int ldc, \
+                                             long long ldc2, int batch, tx_stream_t stream)          \
+    {                                                                                             \
+        return gemm_strided_dev<U>(ta, tb, m, n, k, alpha, A, lda, lda2, B, ldb, ldb2, beta, C,   \
+                                   ldc, ldc2, batch, (cudaStream_t)stream);                       \
+    }                                                                                             \
+    extern "C" int tx_gemm_batched_ptr_dev_##SUF(char ta, char tb, int m, int n, int k,           \
+                                                 const U *alpha, const U *const *Aa, int lda,     \
+                                                 const U *const *Ba, int ldb, const U *beta,      \
+                                                 U *const *Ca, int ldc, int batch,                \
+                                                 tx_stream_t stream)                              \
+    {                                                                                             \
+        return gemm_ptr_dev<U>(ta, tb, m, n, k, alpha, Aa, lda, Ba, ldb, beta, Ca, ldc, batch,    \
+                               (cudaStream_t)stream);                                             \
+    }
+
+TX_DEV(s, float)
+TX_DEV(d, double)
+TX_DEV(c, tx_cfloat)
+TX_DEV(z, tx_cdouble)
 
 TX_STRIDED(s, float)
 TX_STRIDED(d, double)

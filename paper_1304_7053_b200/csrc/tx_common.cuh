@@ -64,6 +64,15 @@ template <> __host__ __device__ __forceinline__ double zero<double>() { return 0
 template <> __host__ __device__ __forceinline__ float2 zero<float2>() { return make_float2(0.f, 0.f); }
 template <> __host__ __device__ __forceinline__ double2 zero<double2>() { return make_double2(0.0, 0.0); }
 
+__device__ __forceinline__ bool is_zero(float v) { return v == 0.f; }
+__device__ __forceinline__ bool is_zero(double v) { return v == 0.0; }
+__device__ __forceinline__ bool is_zero(float2 v) { return v.x == 0.f && v.y == 0.f; }
+__device__ __forceinline__ bool is_zero(double2 v) { return v.x == 0.0 && v.y == 0.0; }
+__device__ __forceinline__ bool is_one(float v) { return v == 1.f; }
+__device__ __forceinline__ bool is_one(double v) { return v == 1.0; }
+__device__ __forceinline__ bool is_one(float2 v) { return v.x == 1.f && v.y == 0.f; }
+__device__ __forceinline__ bool is_one(double2 v) { return v.x == 1.0 && v.y == 0.0; }
+
 // y = a*x (axpby with b == 0: y is never read -- the paper's a1b0 generalised
 // to any alpha) and y = a*x + b*y.
 __device__ __forceinline__ float ax(float a, float x) { return a * x; }

@@ -14,7 +14,10 @@ void fill_ops(TypeTables &t)
     t.gather[OPA][OPB][1][0] = &launch_gather<TxT, OPA, OPB, true, false>;
     t.gather[OPA][OPB][0][1] = &launch_gather<TxT, OPA, OPB, false, true>;
     t.gather[OPA][OPB][1][1] = &launch_gather<TxT, OPA, OPB, true, true>;
-    t.count += 6;
+    t.bulk_dyn_dev[OPA][OPB] = &launch_bulk_dev<TxT, OPA, OPB>;
+    t.gather_dev[OPA][OPB][0] = &launch_gather_dev<TxT, OPA, OPB, false>;
+    t.gather_dev[OPA][OPB][1] = &launch_gather_dev<TxT, OPA, OPB, true>;
+    t.count += 9;
 }
 }  // namespace
 
@@ -35,6 +38,8 @@ void TX_CAT(register_gen_, TX_T)(TypeTables &t)
     t.scale[0][1] = &launch_scale<TxT, false, true>;
     t.scale[1][0] = &launch_scale<TxT, true, false>;
     t.scale[1][1] = &launch_scale<TxT, true, true>;
-    t.count += 4;
+    t.scale_dev[0] = &launch_scale<TxT, false, false, true>;
+    t.scale_dev[1] = &launch_scale<TxT, true, false, true>;
+    t.count += 6;
 }
 }  // namespace tx

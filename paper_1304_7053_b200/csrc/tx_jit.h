@@ -36,8 +36,9 @@ enum JitKind { JIT_BULK = 0, JIT_BULK_PTR = 1, JIT_GATHER = 2, JIT_GATHER_PTR = 
 // caller can use an AOT kernel instead.
 template <class T>
 cudaError_t launch_jit(JitKind kind, Params<T> p, int opa, int opb, bool b0, cudaStream_t st,
-                       int bcast = 0)
+                       int bcast = 0, bool devab = false)
 {
+    if (devab && kind == JIT_BULK_PTR) kind = JIT_GATHER_PTR16;  // no DEVAB bulk_ptr kernel
     if (!jit_available()) return cudaErrorNotSupported;
     const bool cplx = is_cplx<T>::value;
     const bool gather = kind == JIT_GATHER || kind == JIT_GATHER_PTR || kind == JIT_GATHER_PTR16;
@@ -51,7 +52,9 @@ cudaError_t launch_jit(JitKind kind, Params<T> p, int opa, int opb, bool b0, cud
              p.m, p.n, p.k, opa, opb, b0 ? "true" : "false");
     std::string expr = std::string(head) + jit_map_string(mp) + ", " + std::to_string(NT);
     if (gather) expr += kind == JIT_GATHER ? ", false" : (kind == JIT_GATHER_PTR16 ? ", true, true" : ", true");
-    if (kind == JIT_BULK && bcast) expr += ", " + std::to_string(bcast);
+    if (kind == JIT_BULK && (bcast || devab)) expr += ", " + std::to_string(bcast);
+    if (kind == JIT_BULK && devab) expr += ", false, true";
+    if (gather && devab) expr += kind == JIT_GATHER ? ", false, true" : (kind == JIT_GATHER_PTR16 ? ", true" : ", false, true");
     expr += ">";
     CUfunction f = jit_function(expr);
     if (!f) return cudaErrorNotSupported;

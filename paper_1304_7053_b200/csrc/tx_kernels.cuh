@@ -47,6 +47,8 @@ struct Params {
     int S;         // pipeline stages (bulk kernel)
     int ntiles;    // ceil(batch / P)
     T alpha, beta;
+    const T *alpha_dev;  // device-resident alpha / beta (DEVAB kernels), else null
+    const T *beta_dev;
 };
 
 // --------------------------------------------------------------------------
@@ -298,12 +300,32 @@ __device__ __forceinline__ void split_item(int sub, int RB, int CB, int &rb, int
 // as op N (conjugation kept).  Chosen per instance by measurement: it pays off
 // where the column reads of stored A hit one bank group (n = 16 with 8/16-byte
 // elements).  MP must then be an N-style mapping with VA = 1.
+// C <- beta*C (or 0) over pairs [pair0, pair0 + np) of a packed C, no A/B reads
+// (alpha == 0 with device-resident scalars).
+template <class T, int NT>
+__device__ __forceinline__ void scale_packed(T *c, long long elems, T beta, bool b0)
+{
+    for (long long e = threadIdx.x; e < elems; e += NT) {
+        if (b0) {
+            c[e] = zero<T>();
+        } else {
+            T y = c[e];
+            c[e] = axpby(zero<T>(), zero<T>(), beta, y);
+        }
+    }
+}
+
+// DEVAB: alpha and beta are read from device memory at run time (the paper's
+// "host or device pointer"): the kernel is instantiated with
+// B0 = false and decides in-kernel: alpha == 0 -> C <- beta*C without reading
+// A, B (nothing when beta == 1); beta == 0 -> C is neither loaded nor read.
 template <class T, int MS, int NS, int KS, int OPA, int OPB, bool B0, class MP, int NT,
-          int BCAST = 0, bool TRA = false>
+          int BCAST = 0, bool TRA = false, bool DEVAB = false>
 __global__ void __launch_bounds__(NT) bulk_kernel(const Params<T> p)
 {
     constexpr bool BA = (BCAST & 1) != 0, BB = (BCAST & 2) != 0;
     static_assert(!TRA || (OPA != OP_N && BCAST == 0 && MS > 0 && MP::VA == 1), "TRA");
+    static_assert(!DEVAB || (!B0 && !TRA && BCAST == 0), "DEVAB");
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int m = MS ? MS : p.m, n = NS ? NS : p.n, k = KS ? KS : p.k;
     const int SA = m * k, SB = k * n, SC = m * n;
@@ -333,6 +355,22 @@ __global__ void __launch_bounds__(NT) bulk_kernel(const Params<T> p)
     __syncthreads();
     grid_dep_wait();    // PDL: the prologue above overlapped the previous grid's tail
     grid_dep_launch();
+    T alpha = p.alpha, beta = p.beta;
+    bool b0r = B0;
+    if constexpr (DEVAB) {
+        alpha = *p.alpha_dev;
+        beta = *p.beta_dev;
+        b0r = is_zero(beta);
+        if (is_zero(alpha)) {  // C <- beta*C; A and B are never read
+            if (is_one(beta)) return;
+            for (int i = 0; i < my_tiles; ++i) {
+                const long long pair0 = (blockIdx.x + (long long)i * G) * P;
+                const int np = (int)min((long long)P, p.batch - pair0);
+                scale_packed<T, NT>(p.C + pair0 * SC, (long long)np * SC, beta, b0r);
+            }
+            return;
+        }
+    }
     if constexpr (BA || BB) {  // the shared operand(s), once per CTA (any alignment)
         if (BA)
             for (int e = threadIdx.x; e < SA; e += NT) shared_ab[e] = p.A[e];
@@ -347,12 +385,12 @@ __global__ void __launch_bounds__(NT) bulk_kernel(const Params<T> p)
         T *st = stage0 + (long long)(i % S) * stage_elems;
         const uint32_t ba = BA ? 0u : np * SA * (uint32_t)sizeof(T);
         const uint32_t bb = BB ? 0u : np * SB * (uint32_t)sizeof(T);
-        const uint32_t bcin = B0 ? 0u : np * SC * (uint32_t)sizeof(T);
+        const uint32_t bcin = b0r ? 0u : np * SC * (uint32_t)sizeof(T);
         uint64_t *bar = &bars[i % S];
         mbar_arrive_expect_tx(bar, ba + bb + bcin);
         if (!BA) bulk_g2s(st, p.A + pair0 * SA, ba, bar, pol);
         if (!BB) bulk_g2s(st + P * sSA, p.B + pair0 * SB, bb, bar, pol);
-        if (!B0) bulk_g2s(st + P * (sSA + sSB), p.C + pair0 * SC, bcin, bar, pol);
+        if (!b0r) bulk_g2s(st + P * (sSA + sSB), p.C + pair0 * SC, bcin, bar, pol);
     };
 
     if (tid == 0)
@@ -385,6 +423,15 @@ __global__ void __launch_bounds__(NT) bulk_kernel(const Params<T> p)
                     atr + q * (LDT * KS), sB + (BB ? 0 : q * SB), B0 ? nullptr : sC + q * SC,
                     gC + q * SC, m, rb, cb, q, m, n, k, p.alpha, p.beta);
             }
+        } else if (DEVAB && b0r) {  // run-time beta == 0: C is never read
+            for (int w = tid; w < items; w += NT) {
+                const int q = w / TPM;
+                int rb, cb;
+                split_item<MP>(w - q * TPM, RB, CB, rb, cb);
+                micro_tile<T, MS, NS, KS, OPA, OPB, true, MP>(sA + q * SA, sB + q * SB, nullptr,
+                                                              gC + q * SC, m, rb, cb, q, m, n, k,
+                                                              alpha, beta);
+            }
         } else {
             for (int w = tid; w < items; w += NT) {
                 const int q = w / TPM;
@@ -394,7 +441,7 @@ __global__ void __launch_bounds__(NT) bulk_kernel(const Params<T> p)
                                                             sB + (BB ? 0 : q * SB),
                                                             B0 ? nullptr : sC + q * SC,
                                                             gC + q * SC, m, rb, cb, q, m, n, k,
-                                                            p.alpha, p.beta);
+                                                            alpha, beta);
             }
         }
         __syncthreads();  // stage i % S fully consumed before it is refilled
@@ -529,9 +576,10 @@ constexpr int GS = 3;
 // iteration later, so the dependent pointer loads never stall a copy issue.
 // The host caps P at 128 (3 x P <= 4 x NT pointer registers).
 template <class T, int MS, int NS, int KS, int OPA, int OPB, bool B0, class MP, int NT, bool PTR,
-          bool V16 = false>
+          bool V16 = false, bool DEVAB = false>
 __global__ void __launch_bounds__(NT) gather_kernel(const Params<T> p)
 {
+    static_assert(!DEVAB || !B0, "DEVAB");
     constexpr int PR = 4;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int m = MS ? MS : p.m, n = NS ? NS : p.n, k = KS ? KS : p.k;
@@ -599,6 +647,7 @@ __global__ void __launch_bounds__(NT) gather_kernel(const Params<T> p)
             cp_async<sizeof(T)>(dst0 + e, src + row + (long long)ld * col);
         }
     };
+    bool b0r = B0;
     auto issue = [&](int i) {
         const long long pair0 = (blockIdx.x + (long long)i * G) * P;
         const int np = (int)min((long long)P, p.batch - pair0);
@@ -606,16 +655,36 @@ __global__ void __launch_bounds__(NT) gather_kernel(const Params<T> p)
         if constexpr (V16) {
             chunks16(i, 0, st, SA, np, pair0, p.A, p.lda2);
             chunks16(i, 1, st + P * SA, SB, np, pair0, p.B, p.ldb2);
-            if (!B0) chunks16(i, 2, st + P * (SA + SB), SC, np, pair0, p.C, p.ldc2);
+            if (!b0r) chunks16(i, 2, st + P * (SA + SB), SC, np, pair0, p.C, p.ldc2);
         } else {
             elems(i, 0, st, SA, rowsA, p.lda, np, pair0, p.A, p.lda2);
             elems(i, 1, st + P * SA, SB, rowsB, p.ldb, np, pair0, p.B, p.ldb2);
-            if (!B0) elems(i, 2, st + P * (SA + SB), SC, m, p.ldc, np, pair0, p.C, p.ldc2);
+            if (!b0r) elems(i, 2, st + P * (SA + SB), SC, m, p.ldc, np, pair0, p.C, p.ldc2);
         }
     };
 
     grid_dep_wait();
     grid_dep_launch();
+    T alpha = p.alpha, beta = p.beta;
+    if constexpr (DEVAB) {  // device-resident alpha / beta: decided here (see bulk_kernel)
+        alpha = *p.alpha_dev;
+        beta = *p.beta_dev;
+        b0r = is_zero(beta);
+        if (is_zero(alpha)) {
+            if (is_one(beta)) return;
+            for (int i = 0; i < my_tiles; ++i) {
+                const long long pair0 = (blockIdx.x + (long long)i * G) * P;
+                const int np = (int)min((long long)P, p.batch - pair0);
+                for (int e = tid; e < np * SC; e += NT) {
+                    const int q = e / SC, r = e - q * SC;
+                    T *c = (PTR ? p.Cp[pair0 + q] : p.C + (pair0 + q) * p.ldc2) + r % m +
+                           (long long)p.ldc * (r / m);
+                    *c = b0r ? zero<T>() : axpby(zero<T>(), zero<T>(), beta, *c);
+                }
+            }
+            return;
+        }
+    }
     if constexpr (PTR) {
         for (int j = 0; j < GS; ++j) {
             load_regs(j);
@@ -646,9 +715,14 @@ __global__ void __launch_bounds__(NT) gather_kernel(const Params<T> p)
             split_item<MP>(w - q * TPM, RB, CB, rb, cb);
             T *cout = PTR ? const_cast<T *>(ptab[(i % GS) * 3 * P + 2 * P + q])
                           : p.C + (pair0 + q) * p.ldc2;
-            micro_tile<T, MS, NS, KS, OPA, OPB, B0, MP>(sA + q * SA, sB + q * SB,
-                                                     B0 ? nullptr : sC + q * SC, cout, p.ldc, rb,
-                                                     cb, q, m, n, k, p.alpha, p.beta);
+            if (DEVAB && b0r)
+                micro_tile<T, MS, NS, KS, OPA, OPB, true, MP>(sA + q * SA, sB + q * SB, nullptr,
+                                                              cout, p.ldc, rb, cb, q, m, n, k,
+                                                              alpha, beta);
+            else
+                micro_tile<T, MS, NS, KS, OPA, OPB, B0, MP>(sA + q * SA, sB + q * SB,
+                                                         B0 ? nullptr : sC + q * SC, cout, p.ldc,
+                                                         rb, cb, q, m, n, k, alpha, beta);
         }
         __syncthreads();
         if constexpr (PTR) {  // slot i % GS is free: pointers of tile i + GS
@@ -675,11 +749,18 @@ __device__ __forceinline__ double2 scal(double2 b, double2 y)
     return make_double2(b.x * y.x - b.y * y.y, b.x * y.y + b.y * y.x);
 }
 
-template <class T, bool PTR, bool B0>
+template <class T, bool PTR, bool B0, bool DEVAB = false>
 __global__ void __launch_bounds__(256) scale_kernel(const Params<T> p)
 {
     grid_dep_wait();
     grid_dep_launch();
+    T beta = p.beta;
+    bool b0r = B0;
+    if constexpr (DEVAB) {  // k == 0 with device-resident beta
+        beta = *p.beta_dev;
+        if (is_one(beta)) return;
+        b0r = is_zero(beta);
+    }
     const long long mn = (long long)p.m * p.n;
     const long long total = mn * p.batch;
     for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
@@ -689,10 +770,10 @@ __global__ void __launch_bounds__(256) scale_kernel(const Params<T> p)
         const int i = r % p.m, j = r / p.m;
         T *c = PTR ? p.Cp[q] : p.C + q * p.ldc2;
         T &y = c[i + (long long)p.ldc * j];
-        if constexpr (B0)
+        if (b0r)
             y = zero<T>();
         else
-            y = scal(p.beta, y);
+            y = scal(beta, y);
     }
 }
 

@@ -295,3 +295,78 @@ def test_jit_instances_match_aot_generic_bitwise(kind):
         assert np.array_equal(outs[0].view(np.uint8), outs[1].view(np.uint8))
         ref = run_oracle(kind, ta, tb, m, n, k, alpha, beta, A, B, C)
         check(kind, ta, tb, m, n, k, alpha, beta, A, B, C, outs[0], ref)
+
+
+# ------------------------------------------------- device-resident alpha / beta
+def _dev_scalar(kind, v):
+    import torch
+
+    return torch.tensor([v], dtype=torch_dtype(kind), device="cuda")
+
+
+@pytest.mark.parametrize("kind", "sdcz")
+def test_device_alpha_beta(kind):
+    """tx_gemm_batched_dev_* read alpha/beta on the device and decide
+    beta == 0 / alpha == 0 in-kernel: same results as the host-scalar call and the oracle;
+    beta == 0 never reads C (NaN-filled), alpha == 0 never reads A, B (NaN-filled)."""
+    import torch
+
+    ab_gen = _ab(kind, "dev")
+    cases = [ab_gen, (ab_gen[0], 0), (0, ab_gen[1]), (0, 0), (0, 1), (1, 1)]
+    for (m, n, k), pad in (((16, 16, 16), (0, 0)), ((8, 16, 4), (0, 0)), ((5, 7, 3), (1, 2)),
+                           ((6, 6, 0), (0, 0))):
+        for alpha, beta in cases:
+            A, B, C = random_case(kind, m, n, max(k, 1), 613, "N", "T", seed=41, tag="dev", pad=pad)
+            if alpha == 0 or k == 0:
+                A.buf[:] = np.nan
+                B.buf[:] = np.nan
+            if beta == 0:
+                C.buf[C.mask()] = np.nan
+            dA, _ = to_dev(A)
+            dB, _ = to_dev(B)
+            dC, _ = to_dev(C)
+            es = dA.element_size()
+            rc = tx.tx_gemm_batched_dev(kind, "N", "T", m, n, k, _dev_scalar(kind, alpha), dA,
+                                        A.ld, A.ld2, dB, B.ld, B.ld2, _dev_scalar(kind, beta), dC,
+                                        C.ld, C.ld2, C.batch)
+            assert rc == 0, tx.status_string(rc)
+            torch.cuda.synchronize()
+            got = dC.cpu().numpy()
+            ref = run_oracle(kind, "N", "T", m, n, k, alpha, beta, A, B, C)
+            if alpha == 0 or k == 0 or beta == 0:
+                assert np.all(np.isfinite(C.dense(got))) or (beta == 1)
+            C0 = C.dense()
+            if (alpha == 0 or k == 0):
+                # C <- beta*C exactly as the oracle (integer-free but single product per entry)
+                assert np.allclose(C.dense(got).astype(np.complex128), C.dense(ref).astype(np.complex128),
+                                   rtol=1e-6 if kind in "sc" else 1e-14, atol=0, equal_nan=True)
+            else:
+                check(kind, "N", "T", m, n, k, alpha, beta, A, B, C, got, ref)
+            # same as the host-scalar call, bitwise (same kernels' arithmetic)
+            if not (alpha == 0 or k == 0):
+                rc2, got2, _ = run_lib(kind, "N", "T", m, n, k, alpha, beta, A, B, C)
+                assert rc2 == 0
+                assert np.array_equal(got.view(np.uint8), got2.view(np.uint8)), (m, n, k, alpha, beta)
+
+
+@pytest.mark.parametrize("kind", "sdcz")
+def test_device_alpha_beta_pointer_arrays(kind):
+    import torch
+
+    m, n, k = 8, 16, 4
+    alpha, beta = _ab(kind, "devp")
+    A, B, C = random_case(kind, m, n, k, 777, seed=42, tag="devp")
+    dA, _ = to_dev(A)
+    dB, _ = to_dev(B)
+    dC, _ = to_dev(C)
+    es = dA.element_size()
+    perm = np.random.default_rng(5).permutation(C.batch)
+    pa = torch.tensor(A.offsets()[perm] * es + dA.data_ptr(), device="cuda")
+    pb = torch.tensor(B.offsets()[perm] * es + dB.data_ptr(), device="cuda")
+    pc = torch.tensor(C.offsets()[perm] * es + dC.data_ptr(), device="cuda")
+    rc = tx.tx_gemm_batched_ptr_dev(kind, "N", "N", m, n, k, _dev_scalar(kind, alpha), pa, A.ld,
+                                    pb, B.ld, _dev_scalar(kind, beta), pc, C.ld, C.batch)
+    assert rc == 0
+    torch.cuda.synchronize()
+    ref = run_oracle(kind, "N", "N", m, n, k, alpha, beta, A, B, C)
+    check(kind, "N", "N", m, n, k, alpha, beta, A, B, C, dC.cpu().numpy(), ref)
