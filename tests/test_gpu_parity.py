@@ -370,3 +370,50 @@ def test_device_alpha_beta_pointer_arrays(kind):
     torch.cuda.synchronize()
     ref = run_oracle(kind, "N", "N", m, n, k, alpha, beta, A, B, C)
     check(kind, "N", "N", m, n, k, alpha, beta, A, B, C, dC.cpu().numpy(), ref)
+
+
+def test_cuda_graph_capture_and_replay_with_device_scalars():
+    """The calls only enqueue kernels on the given stream, so they can be captured in a
+    CUDA graph (after a warm-up call has built any runtime-specialised instance).  With
+    device-resident alpha/beta, the graph is replayed with new scalars, no re-capture."""
+    import torch
+
+    kind, n, batch = "d", 12, 5000
+    A, B, C = random_case(kind, n, n, n, batch, seed=43, tag="graph")
+    dA, _ = to_dev(A)
+    dB, _ = to_dev(B)
+    dC, _ = to_dev(C)
+    C0 = dC.clone()
+    da, db = _dev_scalar(kind, 0.5), _dev_scalar(kind, -0.25)
+    s = torch.cuda.Stream()
+
+    def call():
+        assert tx.tx_gemm_batched_dev(kind, "T", "N", n, n, n, da, dA, n, n * n, dB, n, n * n, db,
+                                      dC, n, n * n, batch, s) == 0
+        assert tx.tx_gemm_batched(kind, "N", "N", n, n, n, 1.0, dA, n, n * n, dB, n, n * n, 1.0,
+                                  dC, n, n * n, batch, s) == 0
+
+    with torch.cuda.stream(s):
+        call()  # warm-up (JIT instances, occupancy caches)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        call()
+    for alpha, beta in ((0.5, -0.25), (2.0, 0.0), (0.0, 3.0)):
+        dC.copy_(C0)
+        da.fill_(alpha)
+        db.fill_(beta)
+        with torch.cuda.stream(s):
+            g.replay()
+        torch.cuda.synchronize()
+        got = dC.cpu().numpy()
+        ref = C.buf.copy()
+        assert oracle.gemm_batched(kind, "T", "N", n, n, n, alpha, A.buf, n, n * n, B.buf, n, n * n,
+                                   beta, ref, n, n * n, batch) == 0
+        C1 = Operand(kind, n, n, batch, 0)
+        C1.buf[:] = ref
+        ref2 = ref.copy()
+        assert oracle.gemm_batched(kind, "N", "N", n, n, n, 1.0, A.buf, n, n * n, B.buf, n, n * n,
+                                   1.0, ref2, n, n * n, batch) == 0
+        err = np.abs(got - ref2).max() / (np.abs(ref2).max() + 1)
+        assert err < 1e-12, (alpha, beta, err)
