@@ -28,11 +28,46 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-KIND = "s"
-SIZES = (10, 16)
-BATCH = 100_000
-WORKLOAD = ("cfg2: SGEMM 100,000 independent pairs at n=10 and at n=16, op N/N, general "
-            "alpha/beta, packed (minimal leading dimensions)")
+WORKLOADS = {
+    # BASELINE.json configs[1]: the paper's headline K20c workload (the default)
+    "cfg2": dict(kind="s", sizes=(10, 16), batch=100_000, beta0=False, sets=2, scaling="weak",
+                 text="cfg2: SGEMM 100,000 independent pairs at n=10 and at n=16, op N/N, general "
+                      "alpha/beta, packed (minimal leading dimensions)",
+                 l2="2 alternating input sets of 570 MB (> 126 MB L2)"),
+    # configs[0]: small case (latency-bound; reported in us per step)
+    "cfg1": dict(kind="s", sizes=(4,), batch=1_000, beta0=True, sets=1, scaling="weak",
+                 text="cfg1: SGEMM 1,000 pairs of 4x4, N/N, alpha=1, beta=0",
+                 l2="192 KB working set: L2-resident by construction (latency-bound case)"),
+    # configs[4]: D/Z 16x16, 10^7 pairs sharded over the GPUs (strong scaling)
+    "cfg5d": dict(kind="d", sizes=(16,), batch=10_000_000, beta0=False, sets=1, scaling="strong",
+                  text="cfg5: DGEMM 16x16, 10^7 pairs in total split over the GPUs, general alpha/beta",
+                  l2="inputs 61 GB >> 126 MB L2"),
+    "cfg5z": dict(kind="z", sizes=(16,), batch=10_000_000, beta0=False, sets=1, scaling="strong",
+                  text="cfg5: ZGEMM 16x16, 10^7 pairs in total split over the GPUs, general alpha/beta",
+                  l2="inputs 123 GB >> 126 MB L2"),
+}
+KIND, SIZES, BATCH, GLOBAL_BATCH, BETA0, NSETS, SCALING = "s", (10, 16), 100_000, 100_000, False, 2, "weak"
+RANGE = (0, 100_000)
+WORKLOAD, L2NOTE = WORKLOADS["cfg2"]["text"], WORKLOADS["cfg2"]["l2"]
+TYPENAME = {"s": "float", "d": "double", "c": "float2", "z": "double2"}
+DTYPE = {"s": "f32", "d": "f64", "c": "c64 (f32 pairs)", "z": "c128 (f64 pairs)"}
+
+
+def configure(name, world, rank):
+    """Select the workload; per-rank pair range (weak: fixed per rank, strong: split)."""
+    global KIND, SIZES, BATCH, GLOBAL_BATCH, BETA0, NSETS, SCALING, RANGE, WORKLOAD, L2NOTE
+    from paper_1304_7053_b200 import shard
+
+    w = WORKLOADS[name]
+    KIND, SIZES, BETA0, NSETS, SCALING = w["kind"], w["sizes"], w["beta0"], w["sets"], w["scaling"]
+    WORKLOAD, L2NOTE = w["text"], w["l2"]
+    if SCALING == "weak":
+        RANGE = shard.weak_range(w["batch"], rank)
+        GLOBAL_BATCH = w["batch"] * world
+    else:
+        RANGE = shard.strong_range(w["batch"], world, rank)
+        GLOBAL_BATCH = w["batch"]
+    BATCH = RANGE[1] - RANGE[0]
 METRIC = "batched GEMM GFlop/s and HBM GB/s (% of peak) vs size n=1..16, 1-8 B200"
 PAPER_CONTEXT = {"hw": "Tesla K20c", "alpha1_beta0_gflops": {"10": 104, "16": 216},
                  "cite": "PAPER.md:37-38, 757, 763 (Table 1)"}
@@ -125,14 +160,14 @@ def dist_setup(args):
 
 
 def make_inputs(rank, set_id, device):
-    """Seeded synthetic batch for one rank: global pair indices [rank*BATCH, (rank+1)*BATCH)."""
+    """Seeded synthetic batch for one rank: its global pair range RANGE of the workload."""
     import txinputs
     from paper_1304_7053_b200 import shard
 
     out = {}
     for n in SIZES:
         key = lambda name: txinputs.stream_key(txinputs.DEFAULT_SEED, "bench", set_id, KIND, n, name)
-        lo, hi = shard.element_range(shard.weak_range(BATCH, rank), n * n)
+        lo, hi = shard.element_range(RANGE, n * n)
         out[n] = tuple(txinputs.values_torch(KIND, key(nm), lo, hi - lo, device)
                        for nm in ("A", "B", "C"))
     return out
@@ -143,6 +178,8 @@ def scalars():
 
     ka = txinputs.stream_key(txinputs.DEFAULT_SEED, "bench", "alpha")
     kb = txinputs.stream_key(txinputs.DEFAULT_SEED, "bench", "beta")
+    if BETA0:
+        return 1.0, 0.0
     return txinputs.scalar(KIND, ka), txinputs.scalar(KIND, kb)
 
 
@@ -239,14 +276,14 @@ def run_reference(args, world, rank):
         step()
     dt = time.perf_counter() - t0
     flops = sum(model.flops(KIND, n, n, n, pairs * T) for n in SIZES) * args.steps
-    byts = sum(model.bytes_moved(KIND, n, n, n, pairs * T, True, True) for n in SIZES) * args.steps
+    byts = sum(model.bytes_moved(KIND, n, n, n, pairs * T, True, not BETA0) for n in SIZES) * args.steps
     val = flops / dt / 1e9
     line = {"impl": "reference", "metric": METRIC, "value": round(val, 3), "unit": "GFlop/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(dt / args.steps * 1e3, 3), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "scaling": SCALING, "vs_baseline": None, "dtype": DTYPE[KIND], "data": "synthetic",
             "gbps": round(byts / dt / 1e9, 3),
-            "config": {"workload": WORKLOAD, "kind": KIND, "sizes": list(SIZES), "batch": BATCH,
+            "config": {"workload": WORKLOAD, "kind": KIND, "sizes": list(SIZES), "batch": GLOBAL_BATCH,
                        "reference_sample": f"{pairs * T} pairs per size per step"},
             "cpu_baseline": {"value": round(val, 3), "unit": "GFlop/s", "cores": T,
                              "kind": "oracle",
@@ -275,7 +312,7 @@ def run_ours(args, world, rank, local):
     dev = torch.device("cuda", local)
     tx.lib()  # fails loudly if the CUDA library is missing: no fallback
     alpha, beta = scalars()
-    sets = [make_inputs(rank, s, dev) for s in range(2)]
+    sets = [make_inputs(rank, s, dev) for s in range(NSETS)]
     torch.cuda.synchronize()
     stream = torch.cuda.current_stream()
     n_launch = [0]
@@ -290,7 +327,7 @@ def run_ours(args, world, rank, local):
     K, W = args.steps, args.warmup
 
     def step(i):
-        s = sets[i % 2]
+        s = sets[i % NSETS]
         for n in SIZES:
             call(n, *s[n])
 
@@ -323,7 +360,7 @@ def run_ours(args, world, rank, local):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
         for i in range(R):
-            call(n, *sets[i % 2][n])
+            call(n, *sets[i % NSETS][n])
         b.record(stream)
         torch.cuda.synchronize()
         per_launch[n] = a.elapsed_time(b) / R
@@ -331,7 +368,7 @@ def run_ours(args, world, rank, local):
     # the kernel's share of the step, to compare with the ncu launch list
     evs = []
     for i in range(min(K, 50)):
-        s_ = sets[i % 2]
+        s_ = sets[i % NSETS]
         for n in SIZES:
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(stream)
@@ -345,38 +382,41 @@ def run_ours(args, world, rank, local):
         ms = max_over_ranks(ms, dev, args)
 
     flops_step = sum(model.flops(KIND, n, n, n, BATCH) for n in SIZES)
-    bytes_step = sum(model.bytes_moved(KIND, n, n, n, BATCH, True, True) for n in SIZES)
+    bytes_step = sum(model.bytes_moved(KIND, n, n, n, BATCH, True, not BETA0) for n in SIZES)
     value = flops_step * K * world / (ms / 1e3) / 1e9
     gbps = bytes_step * K * world / (ms / 1e3) / 1e9
-    dom = 16
-    dom_bytes = model.bytes_moved(KIND, dom, dom, dom, BATCH, True, True)
+    dom = max(SIZES)
+    dom_bytes = model.bytes_moved(KIND, dom, dom, dom, BATCH, True, not BETA0)
     peak, peak_src = peaks()
     achieved = dom_bytes / (per_launch[dom] / 1e3) / 1e9
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": ncu_traffic(),
-                "kernel": "bulk_kernel<float,16,16,16,N,N,beta!=0>",
+                "kernel": f"bulk_kernel<{TYPENAME[KIND]},{dom},{dom},{dom},N,N,beta{'==' if BETA0 else '!='}0>",
                 "algorithmic_bytes_per_launch": dom_bytes,
                 "launch_ms": round(per_launch[dom], 5),
                 "launch_ms_evented": round(evented[dom], 5),
                 "share_of_step_evented": round(evented[dom] / sum(evented.values()), 4),
                 "timing": f"{R} back-to-back launches, CUDA events at both ends",
                 "peak_source": peak_src,
-                "per_size_gbps": {str(n): round(model.bytes_moved(KIND, n, n, n, BATCH, True, True)
+                "per_size_gbps": {str(n): round(model.bytes_moved(KIND, n, n, n, BATCH, True, not BETA0)
                                                 / (per_launch[n] / 1e3) / 1e9, 1) for n in SIZES}}
 
     # ---- end to end through the host-buffer C-ABI entry (pinned host memory) ----
     e2e = None
     if not args.no_e2e:
-        host = {n: tuple(x.cpu().pin_memory() for x in sets[0][n]) for n in SIZES}
+        # end to end over at most 2*10^5 pairs of the rank's batch (pinned host memory)
+        EB = min(BATCH, 200_000)
+        host = {n: tuple(x[: EB * n * n].cpu().pin_memory() for x in sets[0][n]) for n in SIZES}
+        staging = {n: tuple(torch.empty_like(x, device=dev) for x in host[n]) for n in SIZES}
         h2d = sum((x.numel() * x.element_size()) for n in SIZES for x in host[n])
         d2h = sum(host[n][2].numel() * host[n][2].element_size() for n in SIZES)
 
         def e2e_step():
             for n in SIZES:
                 hA, hB, hC = host[n]
-                dA, dB, dC = sets[1][n]
+                dA, dB, dC = staging[n]
                 rc = tx.tx_gemm_batched_hostio(KIND, "N", "N", n, n, n, alpha, hA, n, n * n, hB, n,
-                                               n * n, beta, hC, n, n * n, BATCH, stream, dA, dB, dC)
+                                               n * n, beta, hC, n, n * n, EB, stream, dA, dB, dC)
                 if rc != 0:
                     raise tx.TxError(rc, tx.status_string(rc))
 
@@ -393,7 +433,9 @@ def run_ours(args, world, rank, local):
         ems = s0.elapsed_time(s1)
         if world > 1:
             ems = max_over_ranks(ems, dev, args)
-        e2e = {"value": round(flops_step * KE * world / (ems / 1e3) / 1e9, 2), "unit": "GFlop/s",
+        flops_e2e = sum(model.flops(KIND, n, n, n, EB) for n in SIZES)
+        e2e = {"value": round(flops_e2e * KE * world / (ems / 1e3) / 1e9, 2), "unit": "GFlop/s",
+               "pairs_per_size_per_step": EB,
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": KE,
                "api": "tx_gemm_batched_hostio_s (host buffers, copies inside the timed region)"}
 
@@ -404,12 +446,13 @@ def run_ours(args, world, rank, local):
     if rank == 0:
         line = {"metric": METRIC, "value": round(value, 2), "unit": "GFlop/s", "n_gpus": world,
                 "steps": K, "warmup": W, "ms_per_step": round(ms / K, 5),
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+                "higher_is_better": True, "scaling": SCALING, "vs_baseline": None,
+                "dtype": DTYPE[KIND],
                 "data": "synthetic (seeded counter-based U[-1,1), txinputs)",
                 "config": {"workload": WORKLOAD, "kind": KIND, "sizes": list(SIZES),
-                           "batch_per_gpu": BATCH, "global_batch": BATCH * world,
-                           "parallelism": f"dp{world} (independent batches, no collective)",
-                           "l2": "2 alternating input sets of 570 MB (> 126 MB L2)"},
+                           "batch_per_gpu": BATCH, "global_batch": GLOBAL_BATCH,
+                           "parallelism": f"dp{world} (independent pairs, no collective)",
+                           "l2": L2NOTE},
                 "gbps": round(gbps, 1), "hbm_frac": round(gbps / peak, 4),
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": launches, "clocks": clocks, "paper_context": PAPER_CONTEXT}
@@ -427,11 +470,15 @@ def main():
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS),
+                    help="cfg2 (default, BASELINE configs[1]), cfg1 (configs[0]), cfg5d/cfg5z "
+                         "(configs[4], 10^7 pairs split over the GPUs)")
     ap.add_argument("--dist-backend", default="nccl", choices=("nccl", "gloo"),
                     help="process-group backend for the barrier / max-over-ranks (gloo: testing "
                          "several ranks on one GPU)")
     args = ap.parse_args()
     world, rank, local = dist_setup(args)
+    configure(args.workload, world, rank)
     if args.impl == "reference":
         run_reference(args, world, rank)  # rank 0 only; other ranks exit 0
         return
