@@ -7,8 +7,11 @@
  *
  *   op(X) = X, X^T or X^* selected by 'N'/'n', 'T'/'t', 'C'/'c' (PAPER.md:240-243,
  *   344-345); for the real types 'C' is the same as 'T'.  C^p is m x n, op(A^p) is
- *   m x k, op(B^p) is k x n; 0 <= m, n, k <= 16 (the paper's
- *   size regime; reading R14).
+ *   m x k, op(B^p) is k x n; 0 <= m, n, k <= 32.  Sizes up to
+ *   16 are the paper's regime and have ahead-of-time size-
+ *   specialised kernels for square shapes; larger ones are the paper's "easily
+ *   extended to larger sizes", served by runtime-
+ *   specialised instances (reading R14).
  *   A is stored m x k when transa = 'N', else k x m; B is stored k x n when
  *   transb = 'N', else n x k (reading R8).  Storage is column-major.
  *
@@ -50,7 +53,7 @@
  * call) is invalid -- nothing is enqueued and C is untouched; > 0 a cudaError_t
  * raised while launching.  Argument checks, in order (strided positions, the
  * pointer call's positions in brackets):
- *   transa -1, transb -2, m -3, n -4, k -5 (outside [0,16]), alpha NULL -6,
+ *   transa -1, transb -2, m -3, n -4, k -5 (outside [0,32]), alpha NULL -6,
  *   beta NULL -13 [-11], lda < max(1, rows of stored A) -8,
  *   ldb < max(1, rows of stored B) -11 [-10], ldc < max(1, m) -15 [-13];
  *   batch_count > 1 (strided only): lda2 < 0 -9, ldb2 < 0 -12, ldc2 < ldc*n -16;
@@ -71,8 +74,8 @@ typedef struct { double re, im; } tx_cdouble;
 /* Same handle as cudaStream_t / CUstream. */
 typedef struct CUstream_st *tx_stream_t;
 
-#define TX_VERSION 10000 /* 1.0.0 */
-#define TX_MAX_DIM 16
+#define TX_VERSION 10100 /* 1.1.0 */
+#define TX_MAX_DIM 32
 
 /* ---- strided batch: TGEMM_multi_uniform. Args 1..18. ---- */
 int tx_gemm_batched_s(char transa, char transb, int m, int n, int k,

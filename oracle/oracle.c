@@ -48,7 +48,7 @@
 typedef struct { float re, im; } o_cfloat;
 typedef struct { double re, im; } o_cdouble;
 
-#define O_MAXDIM 16
+#define O_MAXDIM 32
 
 /* ---------------------------------------------------------------- helpers */
 
@@ -78,7 +78,7 @@ static int ranges_overlap(const void *p, long long np, const void *q, long long 
 /*
  * Argument checks, in the order of DESIGN.md §Boundary (argument positions of
  * the strided call; the pointer call's positions in brackets):
- *   transa -1, transb -2, m -3, n -4, k -5 (each in [0,16]), alpha NULL -6,
+ *   transa -1, transb -2, m -3, n -4, k -5 (each in [0,32]), alpha NULL -6,
  *   beta NULL -13 [-11], lda -8, ldb -11 [-10], ldc -15 [-13],
  *   (batch > 1) lda2 < 0 -9, ldb2 < 0 -12, ldc2 < ldc*n -16  (Fig. 1),
  *   batch < 0 -17 [-14], A NULL -7, B NULL -10 [-9], C NULL -14 [-12],

@@ -119,6 +119,7 @@ template <> struct Api<tx_cdouble> {
     static T dev(const tx_cdouble &v) { return make_double2(v.re, v.im); }
 };
 static_assert(sizeof(tx_cfloat) == sizeof(float2), "layout");
+static_assert(TX_MAX_DIM == TXK_MAX_DIM, "size limit");
 static_assert(sizeof(tx_cdouble) == sizeof(double2), "layout");
 
 // ------------------------------------------------------------- validation
@@ -290,7 +291,7 @@ static int gemm_strided(char ta, char tb, int m, int n, int k, const U *alpha, c
             q.lda2 = SA;
             q.ldb2 = SB;
             q.ldc2 = SC;
-            LaunchFn fn = (m == n && n == k) ? tab.bulk_sq[opa][opb][b0][m - 1] : nullptr;
+            LaunchFn fn = (m == n && n == k && m <= 16) ? tab.bulk_sq[opa][opb][b0][m - 1] : nullptr;
             cudaError_t e = cudaErrorNotSupported;
             path = PATH_BULK;
             if (!fn) {  // no AOT instance for this shape: runtime-specialised instance

@@ -31,6 +31,8 @@ typedef unsigned long long uintptr_t;
 
 namespace tx {
 
+constexpr int TXK_MAX_DIM = 32;  // largest m, n, k (TX_MAX_DIM in include/txgemm.h)
+
 template <class T>
 struct Params {
     const T *A;
@@ -144,7 +146,7 @@ __device__ __forceinline__ void micro_tile(const T *__restrict__ a, const T *__r
     constexpr int VLa = (OPA != OP_N && VA > 1) ? VA : 1;   // A vectors run along l
     constexpr int VLb = (OPB == OP_N && VB > 1) ? VB : 1;   // B vectors run along l
     constexpr int VL = VLa > VLb ? VLa : VLb;
-    constexpr int KMAX = KS ? KS : 16;
+    constexpr int KMAX = KS ? KS : TXK_MAX_DIM;
     const int m = MS ? MS : m_;
     const int n = NS ? NS : n_;
     const int k = KS ? KS : k_;

@@ -29,7 +29,7 @@ def test_library_exports_every_declared_symbol():
 
 
 def test_version_and_instances():
-    assert tx.version() == 10000
+    assert tx.version() == 10100
     assert tx.num_instances() > 800
     assert "success" in tx.status_string(0)
     assert "lda" in tx.status_string(-8)
@@ -57,7 +57,7 @@ def _vec(**kw):
 
 
 BAD = [
-    dict(ta="x"), dict(tb="?"), dict(m=-1), dict(m=17), dict(n=99), dict(k=-3),
+    dict(ta="x"), dict(tb="?"), dict(m=-1), dict(m=33), dict(n=99), dict(k=-3),
     dict(alpha_ptr=False), dict(beta_ptr=False), dict(lda=3), dict(ta="T", k=5, lda=4),
     dict(ldb=2), dict(ldc=1), dict(lda2=-5), dict(ldb2=-1), dict(ldc2=15), dict(batch=-2),
     dict(A=None), dict(B=None), dict(C=None), dict(C=FAKE + 8),  # C overlaps A

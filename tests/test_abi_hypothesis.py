@@ -15,18 +15,18 @@ OPS = st.sampled_from(list("nNtTcCxq "))
 
 
 @settings(max_examples=400, deadline=None)
-@given(kind=st.sampled_from("sdcz"), ta=OPS, tb=OPS, m=st.integers(-2, 18), n=st.integers(-2, 18),
-       k=st.integers(-2, 18), lda=st.integers(-1, 20), ldb=st.integers(-1, 20),
-       ldc=st.integers(-1, 20), lda2=st.integers(-3, 300), ldb2=st.integers(-3, 300),
-       ldc2=st.integers(-3, 300), batch=st.integers(-2, 5), alpha=st.sampled_from([0.0, 1.0, 2.5]),
+@given(kind=st.sampled_from("sdcz"), ta=OPS, tb=OPS, m=st.integers(-2, 34), n=st.integers(-2, 34),
+       k=st.integers(-2, 34), lda=st.integers(-1, 36), ldb=st.integers(-1, 36),
+       ldc=st.integers(-1, 36), lda2=st.integers(-3, 1200), ldb2=st.integers(-3, 1200),
+       ldc2=st.integers(-3, 1200), batch=st.integers(-2, 5), alpha=st.sampled_from([0.0, 1.0, 2.5]),
        beta=st.sampled_from([0.0, 1.0, -0.5]), a_null=st.booleans(), b_null=st.booleans(),
        c_null=st.booleans(), alpha_ptr=st.booleans(), beta_ptr=st.booleans(),
        c_off=st.integers(0, 4000))
 def test_validation_equivalence(kind, ta, tb, m, n, k, lda, ldb, ldc, lda2, ldb2, ldc2, batch, alpha,
                                 beta, a_null, b_null, c_null, alpha_ptr, beta_ptr, c_off):
     es = {"s": 4, "d": 8, "c": 8, "z": 16}[kind]
-    base = np.zeros(8000, dtype=oracle.NP_DTYPE[kind])
-    offs = {"A": 0, "B": 2000, "C": c_off}
+    base = np.zeros(40000, dtype=oracle.NP_DTYPE[kind])
+    offs = {"A": 0, "B": 12000, "C": 24000 - c_off}
 
     def host(name, null):
         return None if null else base.ctypes.data + offs[name] * es

@@ -417,3 +417,24 @@ def test_cuda_graph_capture_and_replay_with_device_scalars():
                                    1.0, ref2, n, n * n, batch) == 0
         err = np.abs(got - ref2).max() / (np.abs(ref2).max() + 1)
         assert err < 1e-12, (alpha, beta, err)
+
+
+# --------------------------------------------------- sizes beyond 16 (NEXT-4)
+@pytest.mark.parametrize("kind", "sdcz")
+@pytest.mark.parametrize("mnk", [(17, 17, 17), (24, 24, 24), (32, 32, 32), (32, 8, 20), (3, 32, 29)],
+                         ids=lambda t: "x".join(map(str, t)))
+def test_sizes_beyond_16(kind, mnk):
+    """m, n, k up to 32 ("easily extended to larger sizes"): packed
+    (runtime-specialised bulk), padded (gather) and both epilogues."""
+    m, n, k = mnk
+    ops = [("N", "N"), ("T", "N"), ("N", "C" if kind in "cz" else "T")]
+    for ta, tb in ops:
+        for general in (False, True):
+            _case(kind, m, n, k, 211, ta, tb, general, "big")
+    A, B, C = random_case(kind, m, n, k, 97, "T", "T", seed=44, tag="bigpad", pad=(1, 3),
+                          c_sentinel=-1.5)
+    alpha, beta = _ab(kind, "bigpad")
+    rc, got, path = run_lib(kind, "T", "T", m, n, k, alpha, beta, A, B, C)
+    assert rc == 0 and path[0] == "gather"
+    ref = run_oracle(kind, "T", "T", m, n, k, alpha, beta, A, B, C)
+    check(kind, "T", "T", m, n, k, alpha, beta, A, B, C, got, ref)

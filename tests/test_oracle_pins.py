@@ -383,8 +383,9 @@ VALIDATION = [
     ("transa", {"ta": "x"}, -1),
     ("transb", {"tb": "Q"}, -2),
     ("m<0", {"m": -1}, -3),
-    ("m>16", {"m": 17}, -3),
-    ("n>16", {"n": 17}, -4),
+    ("m>32", {"m": 33}, -3),
+    ("n>32", {"n": 33}, -4),
+    ("m=17 valid", {"m": 17, "lda": 17, "ldc": 17, "ldc2": 68}, 0),
     ("k<0", {"k": -2}, -5),
     ("alpha NULL", {"alpha_ptr": False}, -6),
     ("beta NULL", {"beta_ptr": False}, -13),
