@@ -19,7 +19,8 @@ int jit_compiled_count();
 CUfunction jit_function(const std::string &name_expr);
 int jit_occupancy(CUfunction f, int nt, int smem);
 cudaError_t jit_launch(CUfunction f, int grid, int nt, int smem, cudaStream_t st, void *params);
-JitMap jit_mapping(int es, bool cplx, int m, int n, int k, int opa, int opb, bool global_c);
+JitMap jit_mapping(int es, bool cplx, int m, int n, int k, int opa, int opb, bool b0,
+                   bool global_c);
 std::string jit_map_string(const JitMap &mp);
 
 template <class T> inline const char *type_name();
@@ -42,7 +43,7 @@ cudaError_t launch_jit(JitKind kind, Params<T> p, int opa, int opb, bool b0, cud
     if (!jit_available()) return cudaErrorNotSupported;
     const bool cplx = is_cplx<T>::value;
     const bool gather = kind == JIT_GATHER || kind == JIT_GATHER_PTR || kind == JIT_GATHER_PTR16;
-    JitMap mp = jit_mapping((int)sizeof(T), cplx, p.m, p.n, p.k, opa, opb,
+    JitMap mp = jit_mapping((int)sizeof(T), cplx, p.m, p.n, p.k, opa, opb, b0,
                             kind != JIT_BULK);
     constexpr int NT = NT_DEFAULT;
     char head[256];
