@@ -21,7 +21,7 @@ from paper_1304_7053_b200 import model  # noqa: E402
 L2 = 126 * 1024 * 1024
 
 
-def run_case(kind, m, n, k, batch, ta, tb, general, reps, peak, layout="strided"):
+def run_case(kind, m, n, k, batch, ta, tb, general, reps, peak, layout="strided", graph=False):
     es = model.ESIZE[kind]
     per_set = es * (m * k + k * n + m * n) * batch
     ptr = layout == "ptr"
@@ -69,6 +69,23 @@ def run_case(kind, m, n, k, batch, ta, tb, general, reps, peak, layout="strided"
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / reps
+    ms_stream = ms
+    if graph:
+        # Device-side rate without the host's per-call cost: the same `reps` calls
+        # captured once into a CUDA graph (PDL edges kept) and replayed.
+        g = torch.cuda.CUDAGraph()
+        s_cap = torch.cuda.Stream()
+        with torch.cuda.stream(s_cap):
+            with torch.cuda.graph(g, stream=s_cap):
+                for i in range(reps):
+                    call(i % R)
+        g.replay()
+        torch.cuda.synchronize()
+        e0.record()
+        g.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / reps
     byts = model.bytes_moved(kind, m, n, k, batch, True, general, shared_a=shA, shared_b=shB)
     if ptr:
         byts_ptr = model.bytes_moved(kind, m, n, k, batch, True, general, pointer_arrays=True)
@@ -78,6 +95,8 @@ def run_case(kind, m, n, k, batch, ta, tb, general, reps, peak, layout="strided"
             "frac_measured": round(gbps / peak, 4),
             "gflops": round(model.flops(kind, m, n, k, batch) / (ms / 1e3) / 1e9, 1),
             "path": tx.last_path()[0], "sets": R, "layout": layout,
+            **({"timing": "cuda graph of back-to-back calls", "us_stream": round(ms_stream * 1e3, 2)}
+               if graph else {}),
             **({"gbps_with_pointers": round(byts_ptr / (ms / 1e3) / 1e9, 1)} if ptr else {})}
 
 
@@ -90,6 +109,8 @@ def main():
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--out", default="")
     ap.add_argument("--shapes", default="", help="m x n x k list, e.g. 8x16x4,16x3x16")
+    ap.add_argument("--graph", action="store_true",
+                    help="time a CUDA-graph replay of the calls (device time, no host launch cost)")
     ap.add_argument("--layout", default="strided", choices=("strided", "ptr", "sharedA", "sharedB"))
     a = ap.parse_args()
     lo, hi = (int(x) for x in a.sizes.split("-")) if "-" in a.sizes else (int(a.sizes),) * 2
@@ -105,7 +126,7 @@ def main():
                         continue
                     for general in (False, True):
                         r = run_case(kind, m, n, k, a.batch, op[0], op[1], general, a.reps, peak,
-                                     a.layout)
+                                     a.layout, a.graph)
                         print(json.dumps(r), flush=True)
                         if out:
                             out.write(json.dumps(r) + "\n")
@@ -117,7 +138,8 @@ def main():
                 if kind in "sd" and "C" in op:
                     continue
                 for general in (False, True):
-                    r = run_case(kind, nn, nn, nn, a.batch, op[0], op[1], general, a.reps, peak)
+                    r = run_case(kind, nn, nn, nn, a.batch, op[0], op[1], general, a.reps, peak,
+                                 graph=a.graph)
                     line = json.dumps(r)
                     print(line, flush=True)
                     if out:
