@@ -6,6 +6,8 @@
 // (packed, aligned; size-specialised when m == n == k) [+ gather tail] | gather
 // kernel (any other strided layout) ; tx_gemm_batched_ptr_<t> -> gather kernel
 // over the pointer arrays.
+#include <cuda.h>  // CUtensorMap types only (the entry point is resolved at run time)
+
 #include <algorithm>
 #include <atomic>
 #include <cstdint>
@@ -185,6 +187,53 @@ static int validate(bool ptr, char ta, char tb, int m, int n, int k, const void 
 }
 
 static bool aligned16(const void *p) { return ((uintptr_t)p & 15u) == 0; }
+
+// ASW tensor map (tx_dispatch.cuh): stored A viewed as `rows` rows of k*es bytes
+// in 8-byte units; rows longer than 128 B are a 3-D view {16 units, regions,
+// rows} so each box covers one 128-byte region of box_rows rows.  128-byte
+// swizzle, zero fill past the last row.  cuTensorMapEncodeTiled is resolved
+// through cudaGetDriverEntryPoint (no link-time libcuda dependency).
+bool encode_tma_rows(TmaDesc *d, const void *base, int es, int k, long long rows, int box_rows)
+{
+    using EncodeFn = CUresult (*)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *,
+                                  const cuuint64_t *, const cuuint64_t *, const cuuint32_t *,
+                                  const cuuint32_t *, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+    static EncodeFn enc = [] {
+        void *f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) !=
+                cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return (EncodeFn) nullptr;
+        return (EncodeFn)f;
+    }();
+    const int row_bytes = k * es;
+    if (!enc || row_bytes % 128 || box_rows < 1 || box_rows > 256 || rows < 1) return false;
+    static_assert(sizeof(CUtensorMap) == sizeof(TmaDesc), "tensor map size");
+    const cuuint32_t regions = (cuuint32_t)(row_bytes / 128);
+    CUtensorMap map;
+    CUresult r;
+    const cuuint32_t estr[3] = {1, 1, 1};
+    if (regions == 1) {
+        const cuuint64_t dims[2] = {16, (cuuint64_t)rows};
+        const cuuint64_t strides[1] = {128};
+        const cuuint32_t box[2] = {16, (cuuint32_t)box_rows};
+        r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, const_cast<void *>(base), dims, strides, box,
+                estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    } else {
+        const cuuint64_t dims[3] = {16, regions, (cuuint64_t)rows};
+        const cuuint64_t strides[2] = {128, (cuuint64_t)row_bytes};
+        const cuuint32_t box[3] = {16, 1, (cuuint32_t)box_rows};
+        r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, const_cast<void *>(base), dims, strides, box,
+                estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    }
+    if (r != CUDA_SUCCESS) return false;
+    std::memcpy(d, &map, sizeof(map));
+    return true;
+}
 
 static int as_status(cudaError_t e) { return e == cudaSuccess ? 0 : (int)e; }
 

@@ -164,6 +164,31 @@ __device__ __forceinline__ void bulk_g2s(void *sdst, const void *gsrc, uint32_t 
         : "memory");
 }
 
+// global -> shared tensor copy (TMA, SASS UTMALDG) of one box of a 2-D / 3-D
+// tensor map, completion counted on an mbarrier.  tmap: generic address of a
+// 128-byte tensor map in parameter space (__grid_constant__ kernel argument).
+// The full box is always written (out-of-bounds rows are zero-filled), so the
+// transaction count of a box is its full size.
+__device__ __forceinline__ void tma_g2s_2d(void *sdst, const void *tmap, int c0, int c1,
+                                           uint64_t *bar, uint64_t pol)
+{
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        ".L2::cache_hint [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(sdst)),
+        "l"(tmap), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(pol)
+        : "memory");
+}
+
+__device__ __forceinline__ void tma_g2s_3d(void *sdst, const void *tmap, int c0, int c1, int c2,
+                                           uint64_t *bar, uint64_t pol)
+{
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        ".L2::cache_hint [%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(smem_u32(sdst)),
+        "l"(tmap), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar)), "l"(pol)
+        : "memory");
+}
+
 // shared -> global bulk copy, tracked by the issuing thread's bulk groups.
 __device__ __forceinline__ void bulk_s2g(void *gdst, const void *ssrc, uint32_t bytes,
                                          uint64_t pol)

@@ -33,6 +33,12 @@ namespace tx {
 
 constexpr int TXK_MAX_DIM = 32;  // largest m, n, k (TX_MAX_DIM in include/txgemm.h)
 
+// A 128-byte TMA tensor map (the CUtensorMap blob, encoded on the host by
+// cuTensorMapEncodeTiled); used by the ASW bulk instances.
+struct alignas(64) TmaDesc {
+    unsigned long long w[16];
+};
+
 template <class T>
 struct Params {
     const T *A;
@@ -51,6 +57,7 @@ struct Params {
     T alpha, beta;
     const T *alpha_dev;  // device-resident alpha / beta (DEVAB kernels), else null
     const T *beta_dev;
+    TmaDesc tma_a;       // ASW instances: tensor map of stored A (see bulk_kernel)
 };
 
 // --------------------------------------------------------------------------
@@ -133,12 +140,18 @@ __device__ __forceinline__ void stv(T *p, const Vec<T, V> &r)
 // scalar, VA = VB = VC = 1).
 // LDAS: leading dimension of A-N in shared memory when it is not m (the padded
 // transposed copy of the TRA path); CONJA >= 0 overrides the conjugation of A.
+// ASW: stored A (op T/C, k*sizeof(T) a multiple of 128 bytes) lies in shared
+// memory as the TMA engine wrote it with the 128-byte swizzle: row i of the
+// matrix (stored column i, k elements) is a 128-byte line (a_rs bytes apart for
+// each further 128 bytes of the row), and its 16-byte chunk c sits at chunk
+// c ^ (i mod 8).  Lanes reading one l of 8 consecutive rows then hit 8
+// different chunks: no bank conflicts, with no transpose pass.
 template <class T, int MS, int NS, int KS, int OPA, int OPB, bool B0, class MP, int LDAS = 0,
-          int CONJA = -1>
+          int CONJA = -1, bool ASW = false>
 __device__ __forceinline__ void micro_tile(const T *__restrict__ a, const T *__restrict__ b,
                                            const T *__restrict__ cin, T *__restrict__ cout,
                                            long long ldo, int rb, int cb, int q, int m_, int n_,
-                                           int k_, T alpha, T beta)
+                                           int k_, T alpha, T beta, int a_rs = 0)
 {
     constexpr int RM = MP::RM, RN = MP::RN;
     constexpr bool CA = CONJA >= 0 ? (CONJA != 0) : (OPA == OP_C), CBc = (OPB == OP_C);
@@ -209,6 +222,22 @@ __device__ __forceinline__ void micro_tile(const T *__restrict__ a, const T *__r
 #pragma unroll
                     for (int e = 0; e < VA; ++e) av[g + e][t] = u.v[e];
                 }
+        } else if constexpr (ASW) {
+            static_assert(OPA != OP_N && KS > 0 && (KS * sizeof(T)) % 128 == 0, "ASW");
+#pragma unroll
+            for (int r = 0; r < RM; ++r) {
+                const char *rowp = reinterpret_cast<const char *>(a) + 128 * ir[r];
+                const int x = (ir[r] & 7) << 4;
+#pragma unroll
+                for (int t = 0; t < VL; t += VLa) {
+                    constexpr int ES = (int)sizeof(T);
+                    const int lb = (l0 + t) * ES;  // compile-time after unrolling
+                    const char *src = rowp + (lb >> 7) * a_rs + (((lb & 127) & ~15) ^ x) + (lb & 15);
+                    const Vec<T, VLa> u = ldv<T, VLa>(reinterpret_cast<const T *>(src));
+#pragma unroll
+                    for (int e = 0; e < VLa; ++e) av[r][t + e] = u.v[e];
+                }
+            }
         } else {
 #pragma unroll
             for (int r = 0; r < RM; ++r)
@@ -321,13 +350,23 @@ __device__ __forceinline__ void scale_packed(T *c, long long elems, T beta, bool
 // "host or device pointer"): the kernel is instantiated with
 // B0 = false and decides in-kernel: alpha == 0 -> C <- beta*C without reading
 // A, B (nothing when beta == 1); beta == 0 -> C is neither loaded nor read.
+// ASW (OPA = T/C, k*sizeof(T) a multiple of 128 B, m = k <= 16): the A tile is
+// loaded with a TMA tensor copy (p.tma_a: stored A as rows of k elements, one
+// row per stored column, 128-byte swizzle) instead of a 1-D bulk copy, so the
+// transposed reads of A are conflict-free without a transpose pass (see
+// micro_tile).  Rows longer than 128 B are split into 128-byte regions, one box
+// each.  Stages are 1024-byte aligned (the swizzle atom); the host caps
+// P*m <= 256 (the box height limit).
 template <class T, int MS, int NS, int KS, int OPA, int OPB, bool B0, class MP, int NT,
-          int BCAST = 0, bool TRA = false, bool DEVAB = false>
-__global__ void __launch_bounds__(NT) bulk_kernel(const Params<T> p)
+          int BCAST = 0, bool TRA = false, bool DEVAB = false, bool ASW = false>
+__global__ void __launch_bounds__(NT) bulk_kernel(const __grid_constant__ Params<T> p)
 {
     constexpr bool BA = (BCAST & 1) != 0, BB = (BCAST & 2) != 0;
     static_assert(!TRA || (OPA != OP_N && BCAST == 0 && MS > 0 && MP::VA == 1), "TRA");
     static_assert(!DEVAB || (!B0 && !TRA && BCAST == 0), "DEVAB");
+    static_assert(!ASW || (OPA != OP_N && BCAST == 0 && !TRA && !DEVAB && MS > 0 && MS == KS &&
+                           (KS * sizeof(T)) % 128 == 0), "ASW");
+    constexpr int NREG = ASW ? (int)(KS * sizeof(T) / 128) : 1;  // 128-byte regions per row
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int m = MS ? MS : p.m, n = NS ? NS : p.n, k = KS ? KS : p.k;
     const int SA = m * k, SB = k * n, SC = m * n;
@@ -336,14 +375,18 @@ __global__ void __launch_bounds__(NT) bulk_kernel(const Params<T> p)
     const int TPM = RB * CB;
     const int P = p.P, S = p.S;
     const int stage_elems = P * (sSA + sSB + (B0 ? 0 : SC));
-    T *stage0 = reinterpret_cast<T *>(smem_raw);
+    T *stage0 = reinterpret_cast<T *>(
+        ASW ? (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023
+            : reinterpret_cast<uintptr_t>(smem_raw));
     T *shared_ab = stage0 + (long long)S * stage_elems;  // broadcast A then B (packed)
+    const int a_rs = P * m * 128;  // ASW: bytes between the 128-byte regions of the A tile
     constexpr int LDT = MS + 1;                          // TRA: padded transposed A
     T *atr = shared_ab + (BA ? SA : 0) + (BB ? SB : 0);
     const int tr_elems = TRA ? P * LDT * k : 0;
     uint64_t *bars = reinterpret_cast<uint64_t *>(
-        smem_raw + (((long long)S * stage_elems + (BA ? SA : 0) + (BB ? SB : 0) + tr_elems) *
-                        sizeof(T) + 15) / 16 * 16);
+        reinterpret_cast<unsigned char *>(stage0) +
+        (((long long)S * stage_elems + (BA ? SA : 0) + (BB ? SB : 0) + tr_elems) * sizeof(T) + 15) /
+            16 * 16);
 
     const int tid = threadIdx.x;
     const int G = gridDim.x;
@@ -385,12 +428,24 @@ __global__ void __launch_bounds__(NT) bulk_kernel(const Params<T> p)
         const long long pair0 = (blockIdx.x + (long long)i * G) * P;
         const int np = (int)min((long long)P, p.batch - pair0);
         T *st = stage0 + (long long)(i % S) * stage_elems;
-        const uint32_t ba = BA ? 0u : np * SA * (uint32_t)sizeof(T);
+        // ASW: a box always lands whole (rows past the batch are zero-filled)
+        const uint32_t ba = BA ? 0u : (ASW ? P : np) * SA * (uint32_t)sizeof(T);
         const uint32_t bb = BB ? 0u : np * SB * (uint32_t)sizeof(T);
         const uint32_t bcin = b0r ? 0u : np * SC * (uint32_t)sizeof(T);
         uint64_t *bar = &bars[i % S];
         mbar_arrive_expect_tx(bar, ba + bb + bcin);
-        if (!BA) bulk_g2s(st, p.A + pair0 * SA, ba, bar, pol);
+        if constexpr (ASW) {
+            if constexpr (NREG == 1) {
+                tma_g2s_2d(st, &p.tma_a, 0, (int)(pair0 * m), bar, pol);
+            } else {
+#pragma unroll
+                for (int h = 0; h < NREG; ++h)
+                    tma_g2s_3d(reinterpret_cast<char *>(st) + h * a_rs, &p.tma_a, 0, h,
+                               (int)(pair0 * m), bar, pol);
+            }
+        } else if (!BA) {
+            bulk_g2s(st, p.A + pair0 * SA, ba, bar, pol);
+        }
         if (!BB) bulk_g2s(st + P * sSA, p.B + pair0 * SB, bb, bar, pol);
         if (!b0r) bulk_g2s(st + P * (sSA + sSB), p.C + pair0 * SC, bcin, bar, pol);
     };
@@ -433,6 +488,16 @@ __global__ void __launch_bounds__(NT) bulk_kernel(const Params<T> p)
                 micro_tile<T, MS, NS, KS, OPA, OPB, true, MP>(sA + q * SA, sB + q * SB, nullptr,
                                                               gC + q * SC, m, rb, cb, q, m, n, k,
                                                               alpha, beta);
+            }
+        } else if constexpr (ASW) {
+            for (int w = tid; w < items; w += NT) {
+                const int q = w / TPM;
+                int rb, cb;
+                split_item<MP>(w - q * TPM, RB, CB, rb, cb);
+                micro_tile<T, MS, NS, KS, OPA, OPB, B0, MP, 0, -1, true>(
+                    reinterpret_cast<const T *>(reinterpret_cast<const char *>(sA) + q * m * 128),
+                    sB + q * SB, B0 ? nullptr : sC + q * SC, gC + q * SC, m, rb, cb, q, m, n, k,
+                    p.alpha, p.beta, a_rs);
             }
         } else {
             for (int w = tid; w < items; w += NT) {

@@ -56,6 +56,12 @@ struct Inst {
     int es, M, N, K;
     char opa, opb;  // 'N' or 'T' (C behaves like T for addressing)
     bool b0;
+    // A read as op N from a padded copy (the TRA path of bulk_kernel): leading
+    // dimension ldas and per-matrix stride sas in elements (0 = packed M, M*K)
+    int ldas = 0, sas = 0;
+    // A (op T) in the TMA 128-byte-swizzled layout of the ASW path: row i of matrix
+    // q is 128-byte line q*M + i of each 128-byte region, chunk c at c ^ (line % 8)
+    bool asw = false;
 };
 
 inline bool valid(const Inst &s, const Map &m)
@@ -66,7 +72,7 @@ inline bool valid(const Inst &s, const Map &m)
     const int RB = blocks(s.M, m.RM), CB = blocks(s.N, m.RN);
     if (m.RM * RB - s.M >= m.RM || m.RN * CB - s.N >= m.RN) return false;
     if (m.VA > 1) {
-        if (SA % m.VA) return false;
+        if (SA % m.VA || s.ldas) return false;  // the padded copy has an odd ld
         if (s.opa == 'N') {
             if (m.RMODE != 0 || m.RM % m.VA || s.M % m.VA) return false;
         } else if (s.K % m.VA)
@@ -141,8 +147,9 @@ inline Cost cost(const Inst &s, const Map &m, int P)
                 const int v = m.VA;
                 for (int g = 0; g < m.RM; g += v)
                     for (int l = l0; l < l0 + VL; ++l) {
+                        const long sa = s.sas ? s.sas : SA, lda_s = s.ldas ? s.ldas : M;
                         for (int ln = 0; ln < 32; ++ln)
-                            addr[ln] = (A0 + (long)q[ln] * SA + row(ln, g) + (long)M * l) * wpe;
+                            addr[ln] = (A0 + (long)q[ln] * sa + row(ln, g) + lda_s * l) * wpe;
                         wf += wavefronts(addr, v * wpe, act);
                         ++ni;
                     }
@@ -150,8 +157,17 @@ inline Cost cost(const Inst &s, const Map &m, int P)
                 const int v = VLa;
                 for (int r = 0; r < m.RM; ++r)
                     for (int l = l0; l < l0 + VL; l += v) {
-                        for (int ln = 0; ln < 32; ++ln)
-                            addr[ln] = (A0 + (long)q[ln] * SA + l + (long)K * row(ln, r)) * wpe;
+                        for (int ln = 0; ln < 32; ++ln) {
+                            if (s.asw) {
+                                const long line = (long)q[ln] * M + row(ln, r);
+                                const long lb = (long)l * s.es, c = lb % 128;
+                                const long byte = (lb / 128) * (long)P * M * 128 + line * 128 +
+                                                  (((c / 16) ^ (line % 8)) * 16) + c % 16;
+                                addr[ln] = A0 + byte / 4;
+                            } else {
+                                addr[ln] = (A0 + (long)q[ln] * SA + l + (long)K * row(ln, r)) * wpe;
+                            }
+                        }
                         wf += wavefronts(addr, v * wpe, act);
                         ++ni;
                     }

@@ -178,6 +178,36 @@ def test_batch_edges(kind, batch):
         _case(kind, n, n, n, batch, "N", "N", True, f"be{batch}")
 
 
+# ---------------------------------------- A tile by TMA tensor copy (ASW)
+@pytest.mark.parametrize("kind", "dcz")
+@pytest.mark.parametrize("batch", [1, 5, 16, 17, 100, 1003])
+def test_transposed_a_tensor_copy_tiles(kind, batch):
+    """n = 16 with op(A) = T/C on 8/16-byte types: the bulk instances may load A with
+    a swizzled TMA tensor copy whose last box runs past the batch (zero-filled).
+    Ragged batches against the oracle, and bitwise against the pointer-array path
+    (a different data mover, same summation order)."""
+    import torch
+
+    for ta in ("T", "C") if kind in "cz" else ("T",):
+        for tb in ("N", "T"):
+            for general in (False, True):
+                err, path, (A, B, C, alpha, beta, got, ref) = _case(
+                    kind, 16, 16, 16, batch, ta, tb, general, f"asw{batch}")
+                assert path[0] in ("bulk", "bulk+tail"), path
+                dA, _ = to_dev(A)
+                dB, _ = to_dev(B)
+                dC, _ = to_dev(C)
+                es = dA.element_size()
+                pa = torch.tensor(A.offsets() * es + dA.data_ptr(), device="cuda")
+                pb = torch.tensor(B.offsets() * es + dB.data_ptr(), device="cuda")
+                pc = torch.tensor(C.offsets() * es + dC.data_ptr(), device="cuda")
+                rc = tx.tx_gemm_batched_ptr(kind, ta, tb, 16, 16, 16, alpha, pa, A.ld, pb, B.ld,
+                                            beta, pc, C.ld, C.batch)
+                assert rc == 0
+                got_ptr = dC.cpu().numpy()
+                assert np.array_equal(got_ptr.view(np.uint8), got.view(np.uint8))
+
+
 # ------------------------------------------------------ pointer-array layout
 @pytest.mark.parametrize("kind", "sdcz")
 def test_pointer_array_equals_strided_and_oracle(kind):

@@ -15,12 +15,15 @@ import txinputs  # noqa: E402
 
 def main():
     uninit = "--uninit-c" in sys.argv
-    for kind, n, batch in (("s", 16, 3000), ("d", 5, 1001), ("c", 8, 517), ("z", 3, 999)):
+    # d16 / z16 with op(A) = T: the TMA tensor-copy (ASW) instances, ragged last box
+    for kind, n, batch in (("s", 16, 3000), ("d", 5, 1001), ("c", 8, 517), ("z", 3, 999),
+                           ("d", 16, 37), ("z", 16, 21)):
+        ta0 = "T" if n == 16 and kind in "dz" else "N"
         e = n * n
         A = txinputs.values_torch(kind, 1, 0, e * batch, "cuda")
         B = txinputs.values_torch(kind, 2, 0, e * batch, "cuda")
         C = torch.empty(e * batch, dtype=A.dtype, device="cuda")  # uninitialised
-        assert tx.tx_gemm_batched(kind, "N", "T", n, n, n, 1.0, A, n, e, B, n, e, 0.0, C, n, e,
+        assert tx.tx_gemm_batched(kind, ta0, "T", n, n, n, 1.0, A, n, e, B, n, e, 0.0, C, n, e,
                                   batch) == 0
         if not uninit:
             assert tx.tx_gemm_batched(kind, "T", "N", n, n, n, 0.5, A, n, e, B, n, e, 0.25, C, n, e,

@@ -20,13 +20,32 @@ from paper_1304_7053_b200 import model  # noqa: E402
 
 L2 = 126 * 1024 * 1024
 
+try:  # SM clock / power-cap state sampled while the timed calls run
+    import pynvml
+
+    pynvml.nvmlInit()
+    _NVH = pynvml.nvmlDeviceGetHandleByIndex(torch.cuda.current_device())
+except Exception:  # pragma: no cover - no NVML
+    _NVH = None
+
+
+def _clock_sample():
+    if _NVH is None:
+        return None
+    try:
+        mhz = pynvml.nvmlDeviceGetClockInfo(_NVH, pynvml.NVML_CLOCK_SM)
+        r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(_NVH)
+        return {"sm_mhz": mhz, "power_cap": bool(r & pynvml.nvmlClocksEventReasonSwPowerCap)}
+    except Exception:
+        return None
+
 
 def run_case(kind, m, n, k, batch, ta, tb, general, reps, peak, layout="strided", graph=False):
     es = model.ESIZE[kind]
     per_set = es * (m * k + k * n + m * n) * batch
     ptr = layout == "ptr"
     shA, shB = layout == "sharedA", layout == "sharedB"
-    R = max(1, min(8, -(-4 * L2 // per_set)))
+    R = max(1, min(64, -(-4 * L2 // per_set)))
     sets = []
     for r in range(R):
         key = lambda nm: txinputs.stream_key(7, "sweep", kind, m, n, k, r, nm)
@@ -67,6 +86,7 @@ def run_case(kind, m, n, k, batch, ta, tb, general, reps, peak, layout="strided"
     for i in range(reps):
         call(i % R)
     e1.record()
+    clk = _clock_sample()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / reps
     ms_stream = ms
@@ -84,6 +104,7 @@ def run_case(kind, m, n, k, batch, ta, tb, general, reps, peak, layout="strided"
         e0.record()
         g.replay()
         e1.record()
+        clk = _clock_sample()
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / reps
     byts = model.bytes_moved(kind, m, n, k, batch, True, general, shared_a=shA, shared_b=shB)
@@ -94,7 +115,7 @@ def run_case(kind, m, n, k, batch, ta, tb, general, reps, peak, layout="strided"
             "batch": batch, "us": round(ms * 1e3, 2), "gbps": round(gbps, 1),
             "frac_measured": round(gbps / peak, 4),
             "gflops": round(model.flops(kind, m, n, k, batch) / (ms / 1e3) / 1e9, 1),
-            "path": tx.last_path()[0], "sets": R, "layout": layout,
+            "path": tx.last_path()[0], "sets": R, "layout": layout, "clock": clk,
             **({"timing": "cuda graph of back-to-back calls", "us_stream": round(ms_stream * 1e3, 2)}
                if graph else {}),
             **({"gbps_with_pointers": round(byts_ptr / (ms / 1e3) / 1e9, 1)} if ptr else {})}
