@@ -141,17 +141,18 @@ __device__ __forceinline__ void stv(T *p, const Vec<T, V> &r)
 // LDAS: leading dimension of A-N in shared memory when it is not m (the padded
 // transposed copy of the TRA path); CONJA >= 0 overrides the conjugation of A.
 // ASW: stored A (op T/C, k*sizeof(T) a multiple of 128 bytes) lies in shared
-// memory as the TMA engine wrote it with the 128-byte swizzle: row i of the
-// matrix (stored column i, k elements) is a 128-byte line (a_rs bytes apart for
-// each further 128 bytes of the row), and its 16-byte chunk c sits at chunk
-// c ^ (i mod 8).  Lanes reading one l of 8 consecutive rows then hit 8
+// memory with the 128-byte swizzle (written so by the TMA engine, or by the
+// gather kernel's copies): row i of the matrix (stored column i, k elements) is
+// a 128-byte line (a_rs bytes apart for each further 128 bytes of the row), and
+// its 16-byte chunk c sits at chunk c ^ ((a_row0 + i) mod 8), a_row0 = the
+// matrix's first line in the region.  Lanes reading one l of 8 consecutive rows then hit 8
 // different chunks: no bank conflicts, with no transpose pass.
 template <class T, int MS, int NS, int KS, int OPA, int OPB, bool B0, class MP, int LDAS = 0,
           int CONJA = -1, bool ASW = false>
 __device__ __forceinline__ void micro_tile(const T *__restrict__ a, const T *__restrict__ b,
                                            const T *__restrict__ cin, T *__restrict__ cout,
                                            long long ldo, int rb, int cb, int q, int m_, int n_,
-                                           int k_, T alpha, T beta, int a_rs = 0)
+                                           int k_, T alpha, T beta, int a_rs = 0, int a_row0 = 0)
 {
     constexpr int RM = MP::RM, RN = MP::RN;
     constexpr bool CA = CONJA >= 0 ? (CONJA != 0) : (OPA == OP_C), CBc = (OPB == OP_C);
@@ -227,7 +228,7 @@ __device__ __forceinline__ void micro_tile(const T *__restrict__ a, const T *__r
 #pragma unroll
             for (int r = 0; r < RM; ++r) {
                 const char *rowp = reinterpret_cast<const char *>(a) + 128 * ir[r];
-                const int x = (ir[r] & 7) << 4;
+                const int x = ((ir[r] + a_row0) & 7) << 4;  // line index within the region
 #pragma unroll
                 for (int t = 0; t < VL; t += VLa) {
                     constexpr int ES = (int)sizeof(T);
@@ -642,11 +643,16 @@ constexpr int GS = 3;
 // i+GS+1 into registers at the end of iteration i and stores them one full
 // iteration later, so the dependent pointer loads never stall a copy issue.
 // The host caps P at 128 (3 x P <= 4 x NT pointer registers).
+// ASWG: op(A) = T/C with k*sizeof(T) a multiple of 128 B: the copies of A are
+// placed in the 128-byte-swizzled layout of micro_tile's ASW accessor (the
+// destination address of each chunk / element is simply computed that way), so
+// the transposed reads of A are conflict-free at no extra cost.
 template <class T, int MS, int NS, int KS, int OPA, int OPB, bool B0, class MP, int NT, bool PTR,
-          bool V16 = false, bool DEVAB = false>
+          bool V16 = false, bool DEVAB = false, bool ASWG = false>
 __global__ void __launch_bounds__(NT) gather_kernel(const Params<T> p)
 {
     static_assert(!DEVAB || !B0, "DEVAB");
+    static_assert(!ASWG || (OPA != OP_N && KS > 0 && (KS * sizeof(T)) % 128 == 0 && !DEVAB), "ASWG");
     constexpr int PR = 4;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int m = MS ? MS : p.m, n = NS ? NS : p.n, k = KS ? KS : p.k;
@@ -661,6 +667,13 @@ __global__ void __launch_bounds__(NT) gather_kernel(const Params<T> p)
     const int tid = threadIdx.x;
     const int G = gridDim.x;
     const int my_tiles = (p.ntiles - (int)blockIdx.x + G - 1) / G;
+    const int a_rs = P * m * 128;  // ASWG: bytes between the 128-byte regions of the A tile
+    // ASWG: byte offset in the A tile of byte pb of stored A^q (packed k x m)
+    auto a_swz = [&](int q, int pb) -> int {
+        const int rb = k * (int)sizeof(T);
+        const int i = pb / rb, lb = pb - i * rb, line = q * m + i;
+        return (lb >> 7) * a_rs + line * 128 + ((((lb & 127) >> 4) ^ (line & 7)) << 4) + (lb & 15);
+    };
 
     // ---- pointer staging (PTR)
     const T *preg[PR];
@@ -696,7 +709,9 @@ __global__ void __launch_bounds__(NT) gather_kernel(const Params<T> p)
             const int q = e / ch, c = e - q * ch;
             const char *src =
                 reinterpret_cast<const char *>(ptr_of(tile, which, q, base, ld2, pair0)) + 16 * c;
-            char *dst = reinterpret_cast<char *>(dst0 + (long long)q * elems) + 16 * c;
+            char *dst = (ASWG && which == 0)
+                            ? reinterpret_cast<char *>(dst0) + a_swz(q, 16 * c)
+                            : reinterpret_cast<char *>(dst0 + (long long)q * elems) + 16 * c;
             if ((reinterpret_cast<uintptr_t>(src) & 15) == 0) {
                 cp_async16_cg(dst, src);
             } else {
@@ -711,7 +726,11 @@ __global__ void __launch_bounds__(NT) gather_kernel(const Params<T> p)
             const int q = e / se, r = e - q * se;
             const int row = r % rows, col = r / rows;
             const T *src = ptr_of(tile, which, q, base, ld2, pair0);
-            cp_async<sizeof(T)>(dst0 + e, src + row + (long long)ld * col);
+            T *dst = (ASWG && which == 0)
+                         ? reinterpret_cast<T *>(reinterpret_cast<char *>(dst0) +
+                                                 a_swz(q, r * (int)sizeof(T)))
+                         : dst0 + e;
+            cp_async<sizeof(T)>(dst, src + row + (long long)ld * col);
         }
     };
     bool b0r = B0;
@@ -786,6 +805,11 @@ __global__ void __launch_bounds__(NT) gather_kernel(const Params<T> p)
                 micro_tile<T, MS, NS, KS, OPA, OPB, true, MP>(sA + q * SA, sB + q * SB, nullptr,
                                                               cout, p.ldc, rb, cb, q, m, n, k,
                                                               alpha, beta);
+            else if constexpr (ASWG)
+                micro_tile<T, MS, NS, KS, OPA, OPB, B0, MP, 0, -1, true>(
+                    reinterpret_cast<const T *>(reinterpret_cast<const char *>(sA) + q * m * 128),
+                    sB + q * SB, B0 ? nullptr : sC + q * SC, cout, p.ldc, rb, cb, q, m, n, k, alpha,
+                    beta, a_rs, q * m);
             else
                 micro_tile<T, MS, NS, KS, OPA, OPB, B0, MP>(sA + q * SA, sB + q * SB,
                                                          B0 ? nullptr : sC + q * SC, cout, p.ldc,

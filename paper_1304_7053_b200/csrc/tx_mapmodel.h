@@ -271,9 +271,10 @@ inline double predict(const Inst &s, const Map &m, const Cost &c, int S, bool cp
 // Compact search (a few thousand candidates): widest valid vectors, ROTN in
 // {0, 1, 2}, S in {2, 3, 4}.  scalar_c: C accessed at arbitrary addresses (VC = 1).
 inline Choice search_fast(int es, bool cplx, int M, int N, int K, char opa, char opb, bool b0,
-                          bool scalar_c)
+                          bool scalar_c, bool asw = false)
 {
     Inst s{es, M, N, K, opa, opb, b0};
+    s.asw = asw;  // A in the 128-byte-swizzled layout (ASW / ASWG kernels)
     const int wpe = es / 4;
     std::vector<int> rms, rns;
     for (int b = 1; b <= M; ++b) {

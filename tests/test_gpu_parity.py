@@ -208,6 +208,46 @@ def test_transposed_a_tensor_copy_tiles(kind, batch):
                 assert np.array_equal(got_ptr.view(np.uint8), got.view(np.uint8))
 
 
+@pytest.mark.parametrize("kind", "dcz")
+def test_swizzled_a_gather_layouts(kind):
+    """Gather instances may place op(A) = T/C copies in the 128-byte-swizzled layout
+    (k * sizeof(T) a multiple of 128 B; m not a multiple of 8 checks the per-matrix
+    line offset): pointer arrays (16-byte chunks, permuted) and a padded strided layout
+    (element copies) against the oracle; pointer arrays bitwise against the packed
+    strided call."""
+    import torch
+
+    shapes = [(16, 3, 16), (5, 3, 16), (12, 7, 16)] + ([(3, 4, 8)] if kind == "z" else [])
+    for (m, n, k) in shapes:
+        for ta in ("T", "C") if kind in "cz" else ("T",):
+            for tb in ("N", "T"):
+                alpha, beta = _ab(kind, f"swg{m}{n}{k}")
+                A, B, C = random_case(kind, m, n, k, 517, ta, tb, seed=5, tag="swg")
+                dA, _ = to_dev(A)
+                dB, _ = to_dev(B)
+                dC, _ = to_dev(C)
+                es = dA.element_size()
+                perm = np.random.default_rng(4).permutation(C.batch)
+                pa = torch.tensor(A.offsets()[perm] * es + dA.data_ptr(), device="cuda")
+                pb = torch.tensor(B.offsets()[perm] * es + dB.data_ptr(), device="cuda")
+                pc = torch.tensor(C.offsets()[perm] * es + dC.data_ptr(), device="cuda")
+                rc = tx.tx_gemm_batched_ptr(kind, ta, tb, m, n, k, alpha, pa, A.ld, pb, B.ld,
+                                            beta, pc, C.ld, C.batch)
+                assert rc == 0
+                got_ptr = dC.cpu().numpy()
+                ref = run_oracle(kind, ta, tb, m, n, k, alpha, beta, A, B, C)
+                check(kind, ta, tb, m, n, k, alpha, beta, A, B, C, got_ptr, ref)
+                # the packed strided call (bulk kernel, plain layout): same sums, same bits
+                rc, got_str, _ = run_lib(kind, ta, tb, m, n, k, alpha, beta, A, B, C)
+                assert rc == 0
+                assert np.array_equal(got_str.view(np.uint8), got_ptr.view(np.uint8))
+                Ap, Bp, Cp = random_case(kind, m, n, k, 517, ta, tb, seed=5, tag="swg", pad=(2, 3))
+                rc, got_pad, path = run_lib(kind, ta, tb, m, n, k, alpha, beta, Ap, Bp, Cp)
+                assert rc == 0 and path[0] == "gather", path
+                refp = run_oracle(kind, ta, tb, m, n, k, alpha, beta, Ap, Bp, Cp)
+                check(kind, ta, tb, m, n, k, alpha, beta, Ap, Bp, Cp, got_pad, refp)
+
+
 # ------------------------------------------------------ pointer-array layout
 @pytest.mark.parametrize("kind", "sdcz")
 def test_pointer_array_equals_strided_and_oracle(kind):
