@@ -12,6 +12,7 @@ namespace tx {
 struct JitMap {
     int RM, RN, RMODE, CMODE, LO, VA, VB, VC, ROTN, S, KB;
     int ASW = 0;  // gather instances: A copies placed in the swizzled layout (ASWG)
+    int BSW = 0;  // ... and B copies (BSWG)
 };
 
 bool jit_available();
@@ -21,7 +22,7 @@ CUfunction jit_function(const std::string &name_expr);
 int jit_occupancy(CUfunction f, int nt, int smem);
 cudaError_t jit_launch(CUfunction f, int grid, int nt, int smem, cudaStream_t st, void *params);
 JitMap jit_mapping(int es, bool cplx, int m, int n, int k, int opa, int opb, bool b0,
-                   bool global_c, bool asw_ok = false);
+                   bool global_c, bool asw_ok = false, bool bsw_ok = false);
 std::string jit_map_string(const JitMap &mp);
 
 template <class T> inline const char *type_name();
@@ -47,8 +48,9 @@ cudaError_t launch_jit(JitKind kind, Params<T> p, int opa, int opb, bool b0, cud
     // swizzled A placement is possible in the gather kernels when a stored column of
     // op(A) = T/C spans whole 128-byte lines
     const bool asw_ok = gather && !devab && opa != OP_N && (p.k * (int)sizeof(T)) % 128 == 0;
+    const bool bsw_ok = gather && !devab && opb == OP_N && (p.k * (int)sizeof(T)) % 128 == 0;
     JitMap mp = jit_mapping((int)sizeof(T), cplx, p.m, p.n, p.k, opa, opb, b0,
-                            kind != JIT_BULK, asw_ok);
+                            kind != JIT_BULK, asw_ok, bsw_ok);
     constexpr int NT = NT_DEFAULT;
     char head[256];
     const char *kname = kind == JIT_BULK ? "bulk_kernel"
@@ -56,11 +58,12 @@ cudaError_t launch_jit(JitKind kind, Params<T> p, int opa, int opb, bool b0, cud
     snprintf(head, sizeof(head), "&tx::%s<%s, %d, %d, %d, %d, %d, %s, ", kname, type_name<T>(),
              p.m, p.n, p.k, opa, opb, b0 ? "true" : "false");
     std::string expr = std::string(head) + jit_map_string(mp) + ", " + std::to_string(NT);
-    if (gather) {  // <..., PTR, V16, DEVAB, ASWG>
+    if (gather) {  // <..., PTR, V16, DEVAB, ASWG, BSWG>
         expr += kind == JIT_GATHER ? ", false" : ", true";
         expr += kind == JIT_GATHER_PTR16 ? ", true" : ", false";
         expr += devab ? ", true" : ", false";
         expr += mp.ASW ? ", true" : ", false";
+        expr += mp.BSW ? ", true" : ", false";
     }
     if (kind == JIT_BULK && (bcast || devab)) expr += ", " + std::to_string(bcast);
     if (kind == JIT_BULK && devab) expr += ", false, true";

@@ -145,14 +145,16 @@ __device__ __forceinline__ void stv(T *p, const Vec<T, V> &r)
 // gather kernel's copies): row i of the matrix (stored column i, k elements) is
 // a 128-byte line (a_rs bytes apart for each further 128 bytes of the row), and
 // its 16-byte chunk c sits at chunk c ^ ((a_row0 + i) mod 8), a_row0 = the
-// matrix's first line in the region.  Lanes reading one l of 8 consecutive rows then hit 8
+// matrix's first line in the region.  BSW: the same for stored B with op N
+// (column j of B, k elements, is line b_row0 + j; regions b_rs bytes apart).  Lanes reading one l of 8 consecutive rows then hit 8
 // different chunks: no bank conflicts, with no transpose pass.
 template <class T, int MS, int NS, int KS, int OPA, int OPB, bool B0, class MP, int LDAS = 0,
-          int CONJA = -1, bool ASW = false>
+          int CONJA = -1, bool ASW = false, bool BSW = false>
 __device__ __forceinline__ void micro_tile(const T *__restrict__ a, const T *__restrict__ b,
                                            const T *__restrict__ cin, T *__restrict__ cout,
                                            long long ldo, int rb, int cb, int q, int m_, int n_,
-                                           int k_, T alpha, T beta, int a_rs = 0, int a_row0 = 0)
+                                           int k_, T alpha, T beta, int a_rs = 0, int a_row0 = 0,
+                                           int b_rs = 0, int b_row0 = 0)
 {
     constexpr int RM = MP::RM, RN = MP::RN;
     constexpr bool CA = CONJA >= 0 ? (CONJA != 0) : (OPA == OP_C), CBc = (OPB == OP_C);
@@ -250,7 +252,23 @@ __device__ __forceinline__ void micro_tile(const T *__restrict__ a, const T *__r
                 }
         }
         // op(B)_{lj}: b[l + k*j] (N) or b[j + n*l] (T/C)
-        if constexpr (OPB == OP_N) {
+        if constexpr (BSW) {
+            static_assert(OPB == OP_N && KS > 0 && (KS * sizeof(T)) % 128 == 0, "BSW");
+#pragma unroll
+            for (int c = 0; c < RN; ++c) {
+                const char *rowp = reinterpret_cast<const char *>(b) + 128 * jc[c];
+                const int x = ((jc[c] + b_row0) & 7) << 4;
+#pragma unroll
+                for (int t = 0; t < VL; t += VLb) {
+                    constexpr int ES = (int)sizeof(T);
+                    const int lb = (l0 + t) * ES;
+                    const char *src = rowp + (lb >> 7) * b_rs + (((lb & 127) & ~15) ^ x) + (lb & 15);
+                    const Vec<T, VLb> u = ldv<T, VLb>(reinterpret_cast<const T *>(src));
+#pragma unroll
+                    for (int e = 0; e < VLb; ++e) bv[c][t + e] = u.v[e];
+                }
+            }
+        } else if constexpr (OPB == OP_N) {
 #pragma unroll
             for (int c = 0; c < RN; ++c)
 #pragma unroll
@@ -646,13 +664,15 @@ constexpr int GS = 3;
 // ASWG: op(A) = T/C with k*sizeof(T) a multiple of 128 B: the copies of A are
 // placed in the 128-byte-swizzled layout of micro_tile's ASW accessor (the
 // destination address of each chunk / element is simply computed that way), so
-// the transposed reads of A are conflict-free at no extra cost.
+// the transposed reads of A are conflict-free at no extra cost.  BSWG: the same
+// for B with op N (its columns are the k-contiguous lines).
 template <class T, int MS, int NS, int KS, int OPA, int OPB, bool B0, class MP, int NT, bool PTR,
-          bool V16 = false, bool DEVAB = false, bool ASWG = false>
+          bool V16 = false, bool DEVAB = false, bool ASWG = false, bool BSWG = false>
 __global__ void __launch_bounds__(NT) gather_kernel(const Params<T> p)
 {
     static_assert(!DEVAB || !B0, "DEVAB");
     static_assert(!ASWG || (OPA != OP_N && KS > 0 && (KS * sizeof(T)) % 128 == 0 && !DEVAB), "ASWG");
+    static_assert(!BSWG || (OPB == OP_N && KS > 0 && (KS * sizeof(T)) % 128 == 0 && !DEVAB), "BSWG");
     constexpr int PR = 4;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int m = MS ? MS : p.m, n = NS ? NS : p.n, k = KS ? KS : p.k;
@@ -669,10 +689,13 @@ __global__ void __launch_bounds__(NT) gather_kernel(const Params<T> p)
     const int my_tiles = (p.ntiles - (int)blockIdx.x + G - 1) / G;
     const int a_rs = P * m * 128;  // ASWG: bytes between the 128-byte regions of the A tile
     // ASWG: byte offset in the A tile of byte pb of stored A^q (packed k x m)
-    auto a_swz = [&](int q, int pb) -> int {
+    const int b_rs = P * n * 128;  // BSWG: the same for the B tile
+    // ASWG / BSWG: byte offset in the A (B) tile of byte pb of stored A^q (B^q),
+    // packed k x m (k x n); lines = stored columns
+    auto swz = [&](int q, int pb, int cols, int rs) -> int {
         const int rb = k * (int)sizeof(T);
-        const int i = pb / rb, lb = pb - i * rb, line = q * m + i;
-        return (lb >> 7) * a_rs + line * 128 + ((((lb & 127) >> 4) ^ (line & 7)) << 4) + (lb & 15);
+        const int i = pb / rb, lb = pb - i * rb, line = q * cols + i;
+        return (lb >> 7) * rs + line * 128 + ((((lb & 127) >> 4) ^ (line & 7)) << 4) + (lb & 15);
     };
 
     // ---- pointer staging (PTR)
@@ -709,9 +732,9 @@ __global__ void __launch_bounds__(NT) gather_kernel(const Params<T> p)
             const int q = e / ch, c = e - q * ch;
             const char *src =
                 reinterpret_cast<const char *>(ptr_of(tile, which, q, base, ld2, pair0)) + 16 * c;
-            char *dst = (ASWG && which == 0)
-                            ? reinterpret_cast<char *>(dst0) + a_swz(q, 16 * c)
-                            : reinterpret_cast<char *>(dst0 + (long long)q * elems) + 16 * c;
+            char *dst = (ASWG && which == 0)   ? reinterpret_cast<char *>(dst0) + swz(q, 16 * c, m, a_rs)
+                        : (BSWG && which == 1) ? reinterpret_cast<char *>(dst0) + swz(q, 16 * c, n, b_rs)
+                                               : reinterpret_cast<char *>(dst0 + (long long)q * elems) + 16 * c;
             if ((reinterpret_cast<uintptr_t>(src) & 15) == 0) {
                 cp_async16_cg(dst, src);
             } else {
@@ -728,7 +751,10 @@ __global__ void __launch_bounds__(NT) gather_kernel(const Params<T> p)
             const T *src = ptr_of(tile, which, q, base, ld2, pair0);
             T *dst = (ASWG && which == 0)
                          ? reinterpret_cast<T *>(reinterpret_cast<char *>(dst0) +
-                                                 a_swz(q, r * (int)sizeof(T)))
+                                                 swz(q, r * (int)sizeof(T), m, a_rs))
+                     : (BSWG && which == 1)
+                         ? reinterpret_cast<T *>(reinterpret_cast<char *>(dst0) +
+                                                 swz(q, r * (int)sizeof(T), n, b_rs))
                          : dst0 + e;
             cp_async<sizeof(T)>(dst, src + row + (long long)ld * col);
         }
@@ -805,11 +831,14 @@ __global__ void __launch_bounds__(NT) gather_kernel(const Params<T> p)
                 micro_tile<T, MS, NS, KS, OPA, OPB, true, MP>(sA + q * SA, sB + q * SB, nullptr,
                                                               cout, p.ldc, rb, cb, q, m, n, k,
                                                               alpha, beta);
-            else if constexpr (ASWG)
-                micro_tile<T, MS, NS, KS, OPA, OPB, B0, MP, 0, -1, true>(
-                    reinterpret_cast<const T *>(reinterpret_cast<const char *>(sA) + q * m * 128),
-                    sB + q * SB, B0 ? nullptr : sC + q * SC, cout, p.ldc, rb, cb, q, m, n, k, alpha,
-                    beta, a_rs, q * m);
+            else if constexpr (ASWG || BSWG)
+                micro_tile<T, MS, NS, KS, OPA, OPB, B0, MP, 0, -1, ASWG, BSWG>(
+                    ASWG ? reinterpret_cast<const T *>(reinterpret_cast<const char *>(sA) + q * m * 128)
+                         : sA + q * SA,
+                    BSWG ? reinterpret_cast<const T *>(reinterpret_cast<const char *>(sB) + q * n * 128)
+                         : sB + q * SB,
+                    B0 ? nullptr : sC + q * SC, cout, p.ldc, rb, cb, q, m, n, k, alpha, beta, a_rs,
+                    q * m, b_rs, q * n);
             else
                 micro_tile<T, MS, NS, KS, OPA, OPB, B0, MP>(sA + q * SA, sB + q * SB,
                                                          B0 ? nullptr : sC + q * SC, cout, p.ldc,

@@ -62,6 +62,7 @@ struct Inst {
     // A (op T) in the TMA 128-byte-swizzled layout of the ASW path: row i of matrix
     // q is 128-byte line q*M + i of each 128-byte region, chunk c at c ^ (line % 8)
     bool asw = false;
+    bool bsw = false;  // B (op N) likewise: column j of matrix q is line q*N + j
 };
 
 inline bool valid(const Inst &s, const Map &m)
@@ -177,8 +178,17 @@ inline Cost cost(const Inst &s, const Map &m, int P)
                 const int v = VLb;
                 for (int cc = 0; cc < m.RN; ++cc)
                     for (int l = l0; l < l0 + VL; l += v) {
-                        for (int ln = 0; ln < 32; ++ln)
-                            addr[ln] = (B0 + (long)q[ln] * SB + l + (long)K * col(ln, cc)) * wpe;
+                        for (int ln = 0; ln < 32; ++ln) {
+                            if (s.bsw) {
+                                const long line = (long)q[ln] * N + col(ln, cc);
+                                const long lb = (long)l * s.es, c = lb % 128;
+                                const long byte = (lb / 128) * (long)P * N * 128 + line * 128 +
+                                                  (((c / 16) ^ (line % 8)) * 16) + c % 16;
+                                addr[ln] = B0 * wpe + byte / 4;
+                            } else {
+                                addr[ln] = (B0 + (long)q[ln] * SB + l + (long)K * col(ln, cc)) * wpe;
+                            }
+                        }
                         wf += wavefronts(addr, v * wpe, act);
                         ++ni;
                     }
@@ -271,10 +281,11 @@ inline double predict(const Inst &s, const Map &m, const Cost &c, int S, bool cp
 // Compact search (a few thousand candidates): widest valid vectors, ROTN in
 // {0, 1, 2}, S in {2, 3, 4}.  scalar_c: C accessed at arbitrary addresses (VC = 1).
 inline Choice search_fast(int es, bool cplx, int M, int N, int K, char opa, char opb, bool b0,
-                          bool scalar_c, bool asw = false)
+                          bool scalar_c, bool asw = false, bool bsw = false)
 {
     Inst s{es, M, N, K, opa, opb, b0};
     s.asw = asw;  // A in the 128-byte-swizzled layout (ASW / ASWG kernels)
+    s.bsw = bsw;  // B likewise (BSWG)
     const int wpe = es / 4;
     std::vector<int> rms, rns;
     for (int b = 1; b <= M; ++b) {

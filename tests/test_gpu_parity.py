@@ -209,17 +209,18 @@ def test_transposed_a_tensor_copy_tiles(kind, batch):
 
 
 @pytest.mark.parametrize("kind", "dcz")
-def test_swizzled_a_gather_layouts(kind):
-    """Gather instances may place op(A) = T/C copies in the 128-byte-swizzled layout
-    (k * sizeof(T) a multiple of 128 B; m not a multiple of 8 checks the per-matrix
-    line offset): pointer arrays (16-byte chunks, permuted) and a padded strided layout
+def test_swizzled_gather_layouts(kind):
+    """Gather instances may place op(A) = T/C and op(B) = N copies in the 128-byte-
+    swizzled layout (k * sizeof(T) a multiple of 128 B; m, n not multiples of 8 check
+    the per-matrix line offset): pointer arrays (16-byte chunks, permuted) and a padded strided layout
     (element copies) against the oracle; pointer arrays bitwise against the packed
     strided call."""
     import torch
 
-    shapes = [(16, 3, 16), (5, 3, 16), (12, 7, 16)] + ([(3, 4, 8)] if kind == "z" else [])
+    shapes = [(16, 3, 16), (5, 3, 16), (12, 7, 16), (1, 16, 16), (4, 6, 16)] + \
+        ([(3, 4, 8)] if kind == "z" else [])
     for (m, n, k) in shapes:
-        for ta in ("T", "C") if kind in "cz" else ("T",):
+        for ta in ("N", "T", "C") if kind in "cz" else ("N", "T"):
             for tb in ("N", "T"):
                 alpha, beta = _ab(kind, f"swg{m}{n}{k}")
                 A, B, C = random_case(kind, m, n, k, 517, ta, tb, seed=5, tag="swg")
