@@ -3,6 +3,7 @@
 
 #include <cuda.h>
 
+#include <algorithm>
 #include <string>
 
 #include "tx_dispatch.cuh"
@@ -47,8 +48,14 @@ cudaError_t launch_jit(JitKind kind, Params<T> p, int opa, int opb, bool b0, cud
     const bool gather = kind == JIT_GATHER || kind == JIT_GATHER_PTR || kind == JIT_GATHER_PTR16;
     // swizzled A placement is possible in the gather kernels when a stored column of
     // op(A) = T/C spans whole 128-byte lines
-    const bool asw_ok = gather && !devab && opa != OP_N && (p.k * (int)sizeof(T)) % 128 == 0;
-    const bool bsw_ok = gather && !devab && opb == OP_N && (p.k * (int)sizeof(T)) % 128 == 0;
+    // bulk: the tile by a TMA tensor copy with the swizzle (ASW / BSW); gather: the
+    // copies placed in the swizzled layout (ASWG / BSWG)
+    // (bulk: k <= 16 only, so the 1024-byte stage alignment never pushes a plan past
+    // the shared-memory limit)
+    const bool swz_kind = gather || (kind == JIT_BULK && !bcast && p.k <= 16);
+    const bool k128 = (p.k * (int)sizeof(T)) % 128 == 0;
+    const bool asw_ok = swz_kind && !devab && opa != OP_N && k128;
+    const bool bsw_ok = swz_kind && !devab && opb == OP_N && k128;
     JitMap mp = jit_mapping((int)sizeof(T), cplx, p.m, p.n, p.k, opa, opb, b0,
                             kind != JIT_BULK, asw_ok, bsw_ok);
     constexpr int NT = NT_DEFAULT;
@@ -65,13 +72,48 @@ cudaError_t launch_jit(JitKind kind, Params<T> p, int opa, int opb, bool b0, cud
         expr += mp.ASW ? ", true" : ", false";
         expr += mp.BSW ? ", true" : ", false";
     }
-    if (kind == JIT_BULK && (bcast || devab)) expr += ", " + std::to_string(bcast);
-    if (kind == JIT_BULK && devab) expr += ", false, true";
+    const bool swz = kind == JIT_BULK && (mp.ASW || mp.BSW);
+    if (kind == JIT_BULK && (bcast || devab || swz)) {  // <..., BCAST, TRA, DEVAB, ASW, BSW>
+        expr += ", " + std::to_string(bcast) + ", false";
+        expr += devab ? ", true" : ", false";
+        expr += mp.ASW ? ", true" : ", false";
+        expr += mp.BSW ? ", true" : ", false";
+    }
     expr += ">";
     CUfunction f = jit_function(expr);
     if (!f) return cudaErrorNotSupported;
+    const int rows_cap = swz ? 256 / std::max(mp.ASW ? p.m : 1, mp.BSW ? p.n : 1) : 0;
     Plan pl = plan_tiles(sizeof(T), p.m, p.n, p.k, b0, mp.RM, mp.RN, NT, p.batch, !gather,
-                         gather ? GS : mp.S, mp.KB, kind == JIT_BULK ? bcast : 0);
+                         gather ? GS : mp.S, mp.KB, kind == JIT_BULK ? bcast : 0, 0, rows_cap);
+    if (swz) {
+        // the 1024-byte alignment of the swizzled regions: shrink the tile until it fits
+        const int es = (int)sizeof(T);
+        const int unit = 16 / gcd_i(16, gcd_i(p.m * p.k * es, gcd_i(p.k * p.n * es, p.m * p.n * es)));
+        auto smem_of = [&](int P) {
+            return swz_smem(pl.S, P, es, p.m, p.n, p.k, b0, mp.ASW != 0, mp.BSW != 0);
+        };
+        // fewer stages first (keeps the tile, i.e. whole passes of the thread block), then P
+        while (smem_of(pl.P) > SMEM_MAX_BYTES && pl.S > 2) --pl.S;
+        while (smem_of(pl.P) > SMEM_MAX_BYTES && pl.P > unit) pl.P -= unit;
+        // two resident CTAs where a full pass of the thread block still fits (one CTA of
+        // 4 warps leaves the copies' latency exposed: ncu, z 16x3x16 TT)
+        const int tpm = ((p.m + mp.RM - 1) / mp.RM) * ((p.n + mp.RN - 1) / mp.RN);
+        const int ppass = std::max(1, NT / tpm);
+        while (smem_of(pl.P) > SMEM_BUDGET_BYTES) {
+            if (pl.P - unit >= ppass) pl.P -= unit;
+            else if (pl.S > 2) --pl.S;
+            else break;
+        }
+        pl.smem = smem_of(pl.P);
+        pl.ntiles = (int)(((long long)p.batch + pl.P - 1) / pl.P);
+        if (pl.smem > SMEM_MAX_BYTES) return cudaErrorNotSupported;
+        if (mp.ASW && !encode_tma_rows(&p.tma_a, p.A, (int)sizeof(T), p.k,
+                                       (long long)p.batch * p.m, pl.P * p.m))
+            return cudaErrorNotSupported;
+        if (mp.BSW && !encode_tma_rows(&p.tma_b, p.B, (int)sizeof(T), p.k,
+                                       (long long)p.batch * p.n, pl.P * p.n))
+            return cudaErrorNotSupported;
+    }
     if (kind == JIT_GATHER_PTR || kind == JIT_GATHER_PTR16)
         gather_ptr_plan(pl, (int)sizeof(T), p.m, p.n, p.k, b0, p.batch);
     if (kind == JIT_BULK_PTR && pl.P > 128) {  // bulk_ptr_kernel: <= 4 pointer triples per lane

@@ -58,6 +58,7 @@ struct Params {
     const T *alpha_dev;  // device-resident alpha / beta (DEVAB kernels), else null
     const T *beta_dev;
     TmaDesc tma_a;       // ASW instances: tensor map of stored A (see bulk_kernel)
+    TmaDesc tma_b;       // BSW instances: tensor map of stored B
 };
 
 // --------------------------------------------------------------------------
@@ -146,8 +147,9 @@ __device__ __forceinline__ void stv(T *p, const Vec<T, V> &r)
 // a 128-byte line (a_rs bytes apart for each further 128 bytes of the row), and
 // its 16-byte chunk c sits at chunk c ^ ((a_row0 + i) mod 8), a_row0 = the
 // matrix's first line in the region.  BSW: the same for stored B with op N
-// (column j of B, k elements, is line b_row0 + j; regions b_rs bytes apart).  Lanes reading one l of 8 consecutive rows then hit 8
-// different chunks: no bank conflicts, with no transpose pass.
+// (column j of B, k elements, is line b_row0 + j; regions b_rs bytes apart).
+// Lanes reading one l of 8 consecutive rows then hit 8 different chunks: no
+// bank conflicts, with no transpose pass.
 template <class T, int MS, int NS, int KS, int OPA, int OPB, bool B0, class MP, int LDAS = 0,
           int CONJA = -1, bool ASW = false, bool BSW = false>
 __device__ __forceinline__ void micro_tile(const T *__restrict__ a, const T *__restrict__ b,
@@ -369,23 +371,28 @@ __device__ __forceinline__ void scale_packed(T *c, long long elems, T beta, bool
 // "host or device pointer"): the kernel is instantiated with
 // B0 = false and decides in-kernel: alpha == 0 -> C <- beta*C without reading
 // A, B (nothing when beta == 1); beta == 0 -> C is neither loaded nor read.
-// ASW (OPA = T/C, k*sizeof(T) a multiple of 128 B, m = k <= 16): the A tile is
-// loaded with a TMA tensor copy (p.tma_a: stored A as rows of k elements, one
-// row per stored column, 128-byte swizzle) instead of a 1-D bulk copy, so the
-// transposed reads of A are conflict-free without a transpose pass (see
-// micro_tile).  Rows longer than 128 B are split into 128-byte regions, one box
-// each.  Stages are 1024-byte aligned (the swizzle atom); the host caps
-// P*m <= 256 (the box height limit).
+// ASW (OPA = T/C, k*sizeof(T) a multiple of 128 B): the A tile is loaded with a
+// TMA tensor copy (p.tma_a: stored A as rows of k elements, one row per stored
+// column, 128-byte swizzle) instead of a 1-D bulk copy, so the transposed reads
+// of A are conflict-free without a transpose pass (see micro_tile).  Rows longer
+// than 128 B are split into 128-byte regions, one box each.  BSW: the same for B
+// with op N (p.tma_b, one row per stored column of B).  The swizzled regions
+// start on 1024-byte boundaries (the swizzle atom); the host caps P*m (P*n) at
+// 256 (the box height limit) and adds the alignment slack to the shared memory.
 template <class T, int MS, int NS, int KS, int OPA, int OPB, bool B0, class MP, int NT,
-          int BCAST = 0, bool TRA = false, bool DEVAB = false, bool ASW = false>
+          int BCAST = 0, bool TRA = false, bool DEVAB = false, bool ASW = false, bool BSW = false>
 __global__ void __launch_bounds__(NT) bulk_kernel(const __grid_constant__ Params<T> p)
 {
     constexpr bool BA = (BCAST & 1) != 0, BB = (BCAST & 2) != 0;
     static_assert(!TRA || (OPA != OP_N && BCAST == 0 && MS > 0 && MP::VA == 1), "TRA");
     static_assert(!DEVAB || (!B0 && !TRA && BCAST == 0), "DEVAB");
-    static_assert(!ASW || (OPA != OP_N && BCAST == 0 && !TRA && !DEVAB && MS > 0 && MS == KS &&
+    static_assert(!ASW || (OPA != OP_N && BCAST == 0 && !TRA && !DEVAB && MS > 0 && KS > 0 &&
                            (KS * sizeof(T)) % 128 == 0), "ASW");
-    constexpr int NREG = ASW ? (int)(KS * sizeof(T) / 128) : 1;  // 128-byte regions per row
+    static_assert(!BSW || (OPB == OP_N && BCAST == 0 && !TRA && !DEVAB && NS > 0 && KS > 0 &&
+                           (KS * sizeof(T)) % 128 == 0), "BSW");
+    constexpr bool SWZ = ASW || BSW;
+    constexpr int ES = (int)sizeof(T);
+    constexpr int NREG = SWZ ? (int)(KS * sizeof(T) / 128) : 1;  // 128-byte regions per row
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int m = MS ? MS : p.m, n = NS ? NS : p.n, k = KS ? KS : p.k;
     const int SA = m * k, SB = k * n, SC = m * n;
@@ -393,12 +400,20 @@ __global__ void __launch_bounds__(NT) bulk_kernel(const __grid_constant__ Params
     const int RB = (m + MP::RM - 1) / MP::RM, CB = (n + MP::RN - 1) / MP::RN;
     const int TPM = RB * CB;
     const int P = p.P, S = p.S;
-    const int stage_elems = P * (sSA + sSB + (B0 ? 0 : SC));
+    // stage: [A tile | B tile | C-in tile], byte offsets.  A swizzled tile is NREG
+    // regions of P*m (P*n) 128-byte lines, each region on a 1024-byte boundary: the
+    // hardware swizzle keys on address bits 7-9, which then equal the line index.
+    const int a_rs = ASW ? ((P * m * 128 + 1023) & ~1023) : P * m * 128;
+    const int b_rs = BSW ? ((P * n * 128 + 1023) & ~1023) : P * n * 128;
+    const int bytesA = ASW ? NREG * a_rs : P * sSA * ES;
+    const int offB = SWZ ? ((bytesA + 1023) & ~1023) : bytesA;
+    const int offC = offB + (BSW ? NREG * b_rs : P * sSB * ES);
+    const int stage_raw = offC + (B0 ? 0 : P * SC * ES);
+    const int stage_elems = (SWZ ? ((stage_raw + 1023) & ~1023) : stage_raw) / ES;
     T *stage0 = reinterpret_cast<T *>(
-        ASW ? (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023
+        SWZ ? (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023
             : reinterpret_cast<uintptr_t>(smem_raw));
     T *shared_ab = stage0 + (long long)S * stage_elems;  // broadcast A then B (packed)
-    const int a_rs = P * m * 128;  // ASW: bytes between the 128-byte regions of the A tile
     constexpr int LDT = MS + 1;                          // TRA: padded transposed A
     T *atr = shared_ab + (BA ? SA : 0) + (BB ? SB : 0);
     const int tr_elems = TRA ? P * LDT * k : 0;
@@ -447,26 +462,36 @@ __global__ void __launch_bounds__(NT) bulk_kernel(const __grid_constant__ Params
         const long long pair0 = (blockIdx.x + (long long)i * G) * P;
         const int np = (int)min((long long)P, p.batch - pair0);
         T *st = stage0 + (long long)(i % S) * stage_elems;
-        // ASW: a box always lands whole (rows past the batch are zero-filled)
+        // ASW / BSW: a box always lands whole (rows past the batch are zero-filled)
         const uint32_t ba = BA ? 0u : (ASW ? P : np) * SA * (uint32_t)sizeof(T);
-        const uint32_t bb = BB ? 0u : np * SB * (uint32_t)sizeof(T);
+        const uint32_t bb = BB ? 0u : (BSW ? P : np) * SB * (uint32_t)sizeof(T);
         const uint32_t bcin = b0r ? 0u : np * SC * (uint32_t)sizeof(T);
         uint64_t *bar = &bars[i % S];
+        char *stb = reinterpret_cast<char *>(st);
         mbar_arrive_expect_tx(bar, ba + bb + bcin);
         if constexpr (ASW) {
             if constexpr (NREG == 1) {
-                tma_g2s_2d(st, &p.tma_a, 0, (int)(pair0 * m), bar, pol);
+                tma_g2s_2d(stb, &p.tma_a, 0, (int)(pair0 * m), bar, pol);
             } else {
 #pragma unroll
                 for (int h = 0; h < NREG; ++h)
-                    tma_g2s_3d(reinterpret_cast<char *>(st) + h * a_rs, &p.tma_a, 0, h,
-                               (int)(pair0 * m), bar, pol);
+                    tma_g2s_3d(stb + h * a_rs, &p.tma_a, 0, h, (int)(pair0 * m), bar, pol);
             }
         } else if (!BA) {
             bulk_g2s(st, p.A + pair0 * SA, ba, bar, pol);
         }
-        if (!BB) bulk_g2s(st + P * sSA, p.B + pair0 * SB, bb, bar, pol);
-        if (!b0r) bulk_g2s(st + P * (sSA + sSB), p.C + pair0 * SC, bcin, bar, pol);
+        if constexpr (BSW) {
+            if constexpr (NREG == 1) {
+                tma_g2s_2d(stb + offB, &p.tma_b, 0, (int)(pair0 * n), bar, pol);
+            } else {
+#pragma unroll
+                for (int h = 0; h < NREG; ++h)
+                    tma_g2s_3d(stb + offB + h * b_rs, &p.tma_b, 0, h, (int)(pair0 * n), bar, pol);
+            }
+        } else if (!BB) {
+            bulk_g2s(stb + offB, p.B + pair0 * SB, bb, bar, pol);
+        }
+        if (!b0r) bulk_g2s(stb + offC, p.C + pair0 * SC, bcin, bar, pol);
     };
 
     if (tid == 0)
@@ -478,8 +503,9 @@ __global__ void __launch_bounds__(NT) bulk_kernel(const __grid_constant__ Params
         const int np = (int)min((long long)P, p.batch - pair0);
         const T *st = stage0 + (long long)(i % S) * stage_elems;
         const T *sA = BA ? shared_ab : st;
-        const T *sB = BB ? shared_ab + (BA ? SA : 0) : st + P * sSA;
-        const T *sC = st + P * (sSA + sSB);
+        const T *sB = BB ? shared_ab + (BA ? SA : 0)
+                         : reinterpret_cast<const T *>(reinterpret_cast<const char *>(st) + offB);
+        const T *sC = reinterpret_cast<const T *>(reinterpret_cast<const char *>(st) + offC);
         T *gC = p.C + pair0 * SC;
         mbar_wait(&bars[i % S], (i / S) & 1);
         const int items = np * TPM;
@@ -508,15 +534,18 @@ __global__ void __launch_bounds__(NT) bulk_kernel(const __grid_constant__ Params
                                                               gC + q * SC, m, rb, cb, q, m, n, k,
                                                               alpha, beta);
             }
-        } else if constexpr (ASW) {
+        } else if constexpr (SWZ) {
             for (int w = tid; w < items; w += NT) {
                 const int q = w / TPM;
                 int rb, cb;
                 split_item<MP>(w - q * TPM, RB, CB, rb, cb);
-                micro_tile<T, MS, NS, KS, OPA, OPB, B0, MP, 0, -1, true>(
-                    reinterpret_cast<const T *>(reinterpret_cast<const char *>(sA) + q * m * 128),
-                    sB + q * SB, B0 ? nullptr : sC + q * SC, gC + q * SC, m, rb, cb, q, m, n, k,
-                    p.alpha, p.beta, a_rs);
+                micro_tile<T, MS, NS, KS, OPA, OPB, B0, MP, 0, -1, ASW, BSW>(
+                    ASW ? reinterpret_cast<const T *>(reinterpret_cast<const char *>(sA) + q * m * 128)
+                        : sA + q * SA,
+                    BSW ? reinterpret_cast<const T *>(reinterpret_cast<const char *>(sB) + q * n * 128)
+                        : sB + q * SB,
+                    B0 ? nullptr : sC + q * SC, gC + q * SC, m, rb, cb, q, m, n, k, p.alpha, p.beta,
+                    a_rs, q * m, b_rs, q * n);
             }
         } else {
             for (int w = tid; w < items; w += NT) {

@@ -52,7 +52,8 @@ def test_square_sweep_all_ops(kind, n):
             assert path[0] in ("bulk", "bulk+tail"), path
 
 
-NONSQUARE = [(8, 16, 4), (16, 3, 16), (1, 16, 16), (16, 16, 1), (5, 7, 3), (16, 1, 7), (2, 9, 13)]
+NONSQUARE = [(8, 16, 4), (16, 3, 16), (1, 16, 16), (16, 16, 1), (5, 7, 3), (16, 1, 7), (2, 9, 13),
+             (5, 6, 16), (12, 7, 16)]
 
 
 @pytest.mark.parametrize("kind", "sdcz")

@@ -39,6 +39,25 @@ def main():
             Cp = torch.zeros((e + 3) * batch, dtype=A.dtype, device="cuda")
             assert tx.tx_gemm_batched(kind, "N", "N", n, n, n, 1.0, A, n, e, B, n, e, 0.5, Cp, n,
                                       e + 3, batch) == 0
+    # runtime-specialised non-square instances with swizzled (TMA tensor) A / B tiles
+    # and the swizzled gather placement (pointer arrays), ragged batches
+    for kind, (m, n, k), ta, tb, batch in (("z", (1, 16, 16), "N", "N", 23),
+                                           ("c", (16, 3, 16), "T", "T", 19),
+                                           ("d", (5, 6, 16), "T", "N", 31)):
+        A = txinputs.values_torch(kind, 4, 0, m * k * batch, "cuda")
+        B = txinputs.values_torch(kind, 5, 0, k * n * batch, "cuda")
+        C = txinputs.values_torch(kind, 6, 0, m * n * batch, "cuda")
+        lda = m if ta == "N" else k
+        ldb = k if tb == "N" else n
+        for beta in (0.0, 0.5):
+            assert tx.tx_gemm_batched(kind, ta, tb, m, n, k, 1.0, A, lda, m * k, B, ldb, k * n, beta,
+                                      C, m, m * n, batch) == 0
+        if not uninit:
+            es = A.element_size()
+            idx = torch.arange(batch, device="cuda")
+            pa, pb, pc = (X.data_ptr() + idx * (s * es) for X, s in ((A, m * k), (B, k * n), (C, m * n)))
+            assert tx.tx_gemm_batched_ptr(kind, ta, tb, m, n, k, 0.5, pa, lda, pb, ldb, 0.25, pc, m,
+                                          batch) == 0
     torch.cuda.synchronize()
     print("ok")
 
