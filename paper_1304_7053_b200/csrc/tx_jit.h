@@ -4,6 +4,7 @@
 #include <cuda.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <string>
 
 #include "tx_dispatch.cuh"
@@ -83,8 +84,13 @@ cudaError_t launch_jit(JitKind kind, Params<T> p, int opa, int opb, bool b0, cud
     CUfunction f = jit_function(expr);
     if (!f) return cudaErrorNotSupported;
     const int rows_cap = swz ? 256 / std::max(mp.ASW ? p.m : 1, mp.BSW ? p.n : 1) : 0;
+    static const int gather_kb = [] {  // TX_GATHER_KB: stage-size target of the gather ring (tuning)
+        const char *v = getenv("TX_GATHER_KB");
+        return v ? atoi(v) : 0;
+    }();
+    const int kb = gather && gather_kb > 0 ? gather_kb : mp.KB;
     Plan pl = plan_tiles(sizeof(T), p.m, p.n, p.k, b0, mp.RM, mp.RN, NT, p.batch, !gather,
-                         gather ? GS : mp.S, mp.KB, kind == JIT_BULK ? bcast : 0, 0, rows_cap);
+                         gather ? GS : mp.S, kb, kind == JIT_BULK ? bcast : 0, 0, rows_cap);
     if (swz) {
         // the 1024-byte alignment of the swizzled regions: shrink the tile until it fits
         const int es = (int)sizeof(T);
