@@ -36,8 +36,9 @@ struct Ty {
 // costs one read and one write of every A element in shared memory plus ~8
 // instructions per element (bulk_kernel TRA).
 static double search_one(const Ty &t, int n, char pa, char pb, bool b0, bool tra, Map &bestm,
-                         Cost &bestc, int &best_S, int qp = 0, bool asw = false)
+                         Cost &bestc, int &best_S, int qp = 0, bool asw = false, bool pc = false)
 {
+    pc = pc || asw;  // the power-capped objective (always for ASW instances)
     const int wpe = t.es / 4;
     const int acc_cap = 64;  // accumulator registers per thread
     Inst s{t.es, n, n, n, tra ? 'N' : pa, pb, b0};
@@ -105,9 +106,9 @@ static double search_one(const Ty &t, int n, char pa, char pb, bool b0, bool tra
                                             const double t_pipe = t_hbm * (S == 2 ? 1.25 : (S == 3 ? 1.05 : 1.0));
                                             const double t_sm = std::max(t_smem, std::max(t_fp, t_issue));
                                             const double tp = std::max(t_pipe, t_sm);
-                                            // ASW: the SM-side time at a power-capped clock (~0.7 x
+                                            // pc: the SM-side time at a power-capped clock (~0.7 x
                                             // max, as sustained runs see) against the HBM time
-                                            const double key = asw ? std::max(t_sm / 0.7, t_pipe) + 0.01 * t_sm + 0.0001 * c.regs
+                                            const double key = pc ? std::max(t_sm / 0.7, t_pipe) + 0.01 * t_sm + 0.0001 * c.regs
                                                                    : tp + 0.001 * c.wf + 0.0001 * c.regs;
                                             if (key < best_key - 1e-9) {
                                                 best_key = key;
@@ -199,6 +200,37 @@ int main(int argc, char **argv)
                                bm.VB, bm.VC, bm.ROTN, bS, bc.wf, bc.ninst, bc.regs, pt);
                         fflush(stdout);
                     }
+        }
+        return 0;
+    }
+    if (argc > 4 && std::strcmp(argv[1], "--pc") == 0) {
+        // re-search square instances of the given types (e.g. "zc") and sizes with the
+        // power-capped objective; TX_MAP lines with S from the search and 16 KB stages
+        const char *kinds = argv[2];
+        const int lo = atoi(argv[3]), hi = atoi(argv[4]);
+        for (auto &t : types) {
+            const char tk = t.es == 4 ? 's' : (t.es == 8 ? (t.cplx ? 'c' : 'd') : 'z');
+            if (!std::strchr(kinds, tk)) continue;
+            for (int n = lo; n <= hi; ++n) {
+                const char *ops = t.cplx ? "NTC" : "NT";
+                for (const char *pa = ops; *pa; ++pa)
+                    for (const char *pb = ops; *pb; ++pb)
+                        for (int b0 = 0; b0 < 2; ++b0) {
+                            const char ca = *pa == 'N' ? 'N' : 'T', cb = *pb == 'N' ? 'N' : 'T';
+                            Map bm{};
+                            Cost bc{};
+                            int bS = 0;
+                            const double pt = search_one(t, n, ca, cb, b0 == 1, false, bm, bc, bS, 0,
+                                                         false, true);
+                            const int opa = *pa == 'N' ? 0 : (*pa == 'T' ? 1 : 2);
+                            const int opb = *pb == 'N' ? 0 : (*pb == 'T' ? 1 : 2);
+                            printf("TX_MAP(%s, %d, %d, %d, %d, %d, %d, %d, %d, %d, %d, %d, %d, %d, %d, 16, 0) "
+                                   "// pc search: wf %.1f inst %.1f regs %d pred %.0f clk/pair\n",
+                                   t.name, n, opa, opb, b0, bm.RM, bm.RN, bm.RMODE, bm.CMODE, bm.LO,
+                                   bm.VA, bm.VB, bm.VC, bm.ROTN, bS, bc.wf, bc.ninst, bc.regs, pt);
+                            fflush(stdout);
+                        }
+            }
         }
         return 0;
     }
