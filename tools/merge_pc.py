@@ -3,7 +3,8 @@ into csrc/tx_map_table.inc where it measured > 1.03 x the current entry, average
 interleaved runs each (cur, pc, cur, pc on one box; tools/gpu_call_r1o.sh).  An op(A) = N
 entry is not replaced when a TRA instance (op(A) = T/C, same op(B) and epilogue, no ASW)
 borrows its mapping (tx_dispatch.cuh TraMap): the c14 NC beta = 0 entry once did, and its
-CC / TC twins fell from 0.85 to 0.52.
+CC / TC twins fell from 0.85 to 0.52.  A TRA entry itself is not replaced either (its measured
+rate came from the candidate N entry's mapping, which may not be merged).
 usage: merge_pc.py CUR1 PC1 CUR2 PC2"""
 import json
 import re
@@ -36,7 +37,8 @@ def main():
         if m:
             t, nn, oa, ob, b0 = m.groups()
             key = (TN[t], int(nn), OPS[int(oa)] + OPS[int(ob)], b0 == "1")
-            if key in c1 and key in p1 and not (oa == "0" and (t, nn, ob, b0) in tra):
+            own_tra = line.split(" //")[0].rstrip().endswith(", 1)") and m.groups()[:5] not in asw
+            if key in c1 and key in p1 and not own_tra and not (oa == "0" and (t, nn, ob, b0) in tra):
                 cur = (c1[key] + c2[key]) / 2
                 new = (p1[key] + p2[key]) / 2
                 if new > 1.03 * cur:
