@@ -89,8 +89,13 @@ cudaError_t launch_jit(JitKind kind, Params<T> p, int opa, int opb, bool b0, cud
         return v ? atoi(v) : 0;
     }();
     const int kb = gather && gather_kb > 0 ? gather_kb : mp.KB;
+    static const bool two_ctas = [] {  // TX_PLAN_2CTA=0: the plain planner (A/B runs)
+        const char *v = getenv("TX_PLAN_2CTA");
+        return !(v && v[0] == '0');
+    }();
     Plan pl = plan_tiles(sizeof(T), p.m, p.n, p.k, b0, mp.RM, mp.RN, NT, p.batch, !gather,
-                         gather ? GS : mp.S, kb, kind == JIT_BULK ? bcast : 0, 0, rows_cap);
+                         gather ? GS : mp.S, kb, kind == JIT_BULK ? bcast : 0, 0, rows_cap,
+                         kind == JIT_BULK && two_ctas);
     if (swz) {
         // the 1024-byte alignment of the swizzled regions: shrink the tile until it fits
         const int es = (int)sizeof(T);
