@@ -250,6 +250,53 @@ def test_swizzled_gather_layouts(kind):
                 check(kind, ta, tb, m, n, k, alpha, beta, Ap, Bp, Cp, got_pad, refp)
 
 
+@pytest.mark.parametrize("kind", "sdcz")
+@pytest.mark.parametrize("batch", [1, 37, 1003])
+def test_pointer_arrays_odd_sizes_any_alignment(kind, batch):
+    """Packed matrices whose byte sizes are not multiples of 16, at arbitrary element
+    offsets (so every 16-byte alignment occurs): the covering-chunk gather (U16) reads
+    partial first / last chunks element by element.  Against the oracle's pointer
+    variant on the same offsets; C entries outside the matrices stay untouched."""
+    import torch
+
+    rng = np.random.default_rng(batch)
+    for (m, n, k) in ((5, 7, 3), (3, 3, 3), (1, 1, 1), (7, 2, 5)):
+        for ta, tb in (("N", "N"), ("T", "C" if kind in "cz" else "T")):
+            for general in (False, True):
+                ra, ca = (m, k) if ta == "N" else (k, m)
+                rb, cb = (k, n) if tb == "N" else (n, k)
+                sa, sb, sc = ra * ca, rb * cb, m * n
+                # each matrix at a random element offset: gaps of 0..7 elements
+                def offs(size):
+                    gaps = rng.integers(0, 8, batch)
+                    return np.cumsum(gaps + size) - size
+                oa, ob, oc = offs(sa), offs(sb), offs(sc)
+                key = lambda nm: txinputs.stream_key(9, "u16", kind, m, n, k, ta, tb, batch, nm)
+                hA = txinputs.values_numpy(kind, key("A"), 0, int(oa[-1]) + sa + 8)
+                hB = txinputs.values_numpy(kind, key("B"), 0, int(ob[-1]) + sb + 8)
+                hC = txinputs.values_numpy(kind, key("C"), 0, int(oc[-1]) + sc + 8)
+                alpha, beta = _ab(kind, f"u16{m}{n}{k}", general)
+                dA, dB, dC = (torch.from_numpy(x.copy()).cuda() for x in (hA, hB, hC))
+                es = dA.element_size()
+                pa = torch.tensor(oa * es + dA.data_ptr(), device="cuda")
+                pb = torch.tensor(ob * es + dB.data_ptr(), device="cuda")
+                pc = torch.tensor(oc * es + dC.data_ptr(), device="cuda")
+                rc = tx.tx_gemm_batched_ptr(kind, ta, tb, m, n, k, alpha, pa, ra, pb, rb, beta, pc,
+                                            m, batch)
+                assert rc == 0
+                got = dC.cpu().numpy()
+                ref = hC.copy()
+                assert oracle.gemm_batched_ptr(kind, ta, tb, m, n, k, alpha, hA, oa, ra, hB, ob, rb,
+                                               beta, ref, oc, m, batch) == 0
+                mask = np.zeros(len(hC), bool)
+                for o in oc:
+                    mask[o:o + sc] = True
+                assert np.array_equal(got[~mask].view(np.uint8), hC[~mask].view(np.uint8))
+                scale = (np.abs(alpha) * k + np.abs(beta)) * 1.0  # |entries| < 1
+                err = np.max(np.abs(got[mask].astype(np.complex128) - ref[mask].astype(np.complex128)))
+                assert err / scale <= (1e-5 if kind in "sc" else 1e-13), (m, n, k, ta, tb, err)
+
+
 # ------------------------------------------------------ pointer-array layout
 @pytest.mark.parametrize("kind", "sdcz")
 def test_pointer_array_equals_strided_and_oracle(kind):

@@ -1,0 +1,11 @@
+# Final validation of the committed library: smoke, all GPU tests, bench, sanitizers.
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo smoke rc=$?; tail -2 gpurun_out/smoke.log
+timeout 1800 python -m pytest tests -m gpu -q > gpurun_out/pytest_all.log 2>&1; echo pytest rc=$?; tail -2 gpurun_out/pytest_all.log
+timeout 300 python bench.py > gpurun_out/bench_default.log 2>&1; echo bench rc=$?; tail -1 gpurun_out/bench_default.log | cut -c1-200
+python tools/sanitize_case.py > /dev/null 2>&1
+for tool in memcheck synccheck racecheck; do
+  timeout 600 compute-sanitizer --tool $tool --error-exitcode 9 python tools/sanitize_case.py > gpurun_out/san3_$tool.log 2>&1; echo $tool rc=$?; tail -1 gpurun_out/san3_$tool.log
+done
+timeout 600 compute-sanitizer --tool initcheck --error-exitcode 9 python tools/sanitize_case.py --uninit-c > gpurun_out/san3_initcheck.log 2>&1; echo initcheck rc=$?; tail -1 gpurun_out/san3_initcheck.log
