@@ -119,7 +119,8 @@ int tx_gemm_batched_ptr_z(char transa, char transb, int m, int n, int k,
  * same layouts (offsets and extents) as hA, hB, hC.  Enqueues on `stream`:
  * host->device copies of the A and B extents (and of C's extent when
  * beta != 0), the GEMM on the device copies, and the device->host copy of C's
- * extent back into hC.  The batch is processed in chunks of ~32 MB: host->device
+ * extent back into hC.  The batch is processed in chunks of ~64 MB of traffic
+ * (TX_HOSTIO_CHUNK_MB overrides; 4-512 MB measured, 64 best): host->device
  * copies run on an internal copy stream, device->host copies on another, the
  * GEMMs on `stream`, ordered by events, so both PCIe directions and the kernels
  * overlap; work already queued on `stream` is ordered before the first copy and

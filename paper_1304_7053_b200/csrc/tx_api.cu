@@ -12,6 +12,7 @@
 #include <atomic>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -605,6 +606,8 @@ static CopyStreams copy_streams()
     return c;
 }
 
+constexpr long long HOSTIO_CHUNK_MB = 64;  // pipeline chunk of the host-buffer entry (measured: 4-512 MB)
+
 template <class U>
 static int gemm_hostio(char ta, char tb, int m, int n, int k, const U *alpha, const U *hA, int lda,
                        long long lda2, const U *hB, int ldb, long long ldb2, const U *beta, U *hC,
@@ -629,9 +632,15 @@ static int gemm_hostio(char ta, char tb, int m, int n, int k, const U *alpha, co
     const int rowsB = op_n(tb) ? k : n, colsB = op_n(tb) ? n : k;
     const size_t es = sizeof(U);
     const bool read_c = !AT::zero(b);
-    // Chunks of whole pairs (~32 MB of traffic each); ld2 == 0 operands are copied once.
+    // Chunks of whole pairs (HOSTIO_CHUNK_MB of traffic each, TX_HOSTIO_CHUNK_MB overrides);
+    // ld2 == 0 operands are copied once.
+    static const long long chunk_bytes = [] {
+        const char *v = getenv("TX_HOSTIO_CHUNK_MB");
+        const long long mb = v ? atoll(v) : HOSTIO_CHUNK_MB;
+        return (mb > 0 ? mb : HOSTIO_CHUNK_MB) << 20;
+    }();
     const long long per_pair = (long long)es * ((reads_ab ? lda2 + ldb2 : 0) + ldc2 * (read_c ? 2 : 1));
-    long long chunk = per_pair > 0 ? (32ll << 20) / per_pair : batch;
+    long long chunk = per_pair > 0 ? chunk_bytes / per_pair : batch;
     if (chunk < 1) chunk = 1;
     const int nchunks = (int)((batch + chunk - 1) / chunk);
     CopyStreams cs = copy_streams();
