@@ -557,3 +557,35 @@ def test_sizes_beyond_16(kind, mnk):
     assert rc == 0 and path[0] == "gather"
     ref = run_oracle(kind, "T", "T", m, n, k, alpha, beta, A, B, C)
     check(kind, "T", "T", m, n, k, alpha, beta, A, B, C, got, ref)
+
+
+@pytest.mark.parametrize("kind", "sdcz")
+@pytest.mark.parametrize("mnk", [(32, 32, 32), (24, 8, 32), (5, 30, 32)],
+                         ids=lambda t: "x".join(map(str, t)))
+def test_pointer_arrays_beyond_16(kind, mnk):
+    """Pointer arrays at sizes 17-32 with k * sizeof(T) a multiple of 128 B (swizzled
+    gather placement possible for op(A) = T/C and op(B) = N): permuted pointers,
+    against the oracle and bitwise against the packed strided call."""
+    import torch
+
+    m, n, k = mnk
+    for ta, tb in (("N", "N"), ("T", "N"), ("C" if kind in "cz" else "T", "T")):
+        A, B, C = random_case(kind, m, n, k, 129, ta, tb, seed=12, tag="ptrbig")
+        alpha, beta = _ab(kind, f"ptrbig{m}{n}{k}")
+        rc, got_strided, _ = run_lib(kind, ta, tb, m, n, k, alpha, beta, A, B, C)
+        assert rc == 0
+        perm = np.random.default_rng(6).permutation(C.batch)
+        dA, _ = to_dev(A)
+        dB, _ = to_dev(B)
+        dC, _ = to_dev(C)
+        es = dA.element_size()
+        pa = torch.tensor(A.offsets()[perm] * es + dA.data_ptr(), device="cuda")
+        pb = torch.tensor(B.offsets()[perm] * es + dB.data_ptr(), device="cuda")
+        pc = torch.tensor(C.offsets()[perm] * es + dC.data_ptr(), device="cuda")
+        rc = tx.tx_gemm_batched_ptr(kind, ta, tb, m, n, k, alpha, pa, A.ld, pb, B.ld, beta, pc,
+                                    C.ld, C.batch)
+        assert rc == 0
+        got = dC.cpu().numpy()
+        assert np.array_equal(got.view(np.uint8), got_strided.view(np.uint8))
+        ref = run_oracle(kind, ta, tb, m, n, k, alpha, beta, A, B, C)
+        check(kind, ta, tb, m, n, k, alpha, beta, A, B, C, got, ref)
