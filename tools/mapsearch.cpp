@@ -134,8 +134,8 @@ int main(int argc, char **argv)
         char line[512];
         printf("// Generated by tools/mapsearch.cpp --tra -- do not edit.  Compute mapping of the\n");
         printf("// TRA instances (A transposed at staging into a padded N-layout copy, ld = n + 1).\n");
-        printf("// TX_TRAMAP(T, n, OPA, OPB, B0, RM, RN, RMODE, CMODE, LO, VA, VB, VC, ROTN, QP)\n");
-        printf("// QP: extra elements between consecutive matrices of the copy (bank shift)\n");
+        printf("// TX_TRAMAP(T, n, OPA, OPB, B0, RM, RN, RMODE, CMODE, LO, VA, VB, VC, ROTN, S, ON)\n");
+        printf("// ON: set by measurement (tools/merge_tra.py)\n");
         while (std::fgets(line, sizeof line, f)) {
             char tn[16];
             int v[16];
@@ -153,7 +153,7 @@ int main(int argc, char **argv)
             Cost bc{};
             int bS = 0, bq = 0;
             double pt = 1e18;
-            for (int qp : {0, 1, 2, 3}) {
+            for (int qp : {0}) {  // the kernel's padded copy has no per-matrix pad (QP = 0)
                 Map m{};
                 Cost c{};
                 int S = 0;
@@ -166,10 +166,11 @@ int main(int argc, char **argv)
                     bq = qp;
                 }
             }
-            printf("TX_TRAMAP(%s, %d, %d, %d, %d, %d, %d, %d, %d, %d, %d, %d, %d, %d, %d) "
+            (void)bq;
+            printf("TX_TRAMAP(%s, %d, %d, %d, %d, %d, %d, %d, %d, %d, %d, %d, %d, %d, %d, 1) "
                    "// wf %.1f inst %.1f regs %d pred %.0f clk/pair (own entry RM %d RN %d)\n",
                    t->name, n, v[1], v[2], v[3], bm.RM, bm.RN, bm.RMODE, bm.CMODE, bm.LO, bm.VA,
-                   bm.VB, bm.VC, bm.ROTN, bq, bc.wf, bc.ninst, bc.regs, pt, v[4], v[5]);
+                   bm.VB, bm.VC, bm.ROTN, bS, bc.wf, bc.ninst, bc.regs, pt, v[4], v[5]);
         }
         std::fclose(f);
         return 0;
