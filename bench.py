@@ -1,24 +1,38 @@
 #!/usr/bin/env python
 """Benchmark of the batched small-matrix GEMM hot path (BASELINE.json).
 
-Workload (BASELINE.json configs[1], the paper's headline K20c workload): SGEMM,
-100,000 independent pairs at n = 10 and at n = 16, N/N, general alpha and beta,
-packed layout.  One step = one pass of the whole hot path over one batch of each
-size (two library calls).  Two input sets (1.14 GB) alternate between steps, so
-a step never finds its inputs in the 126 MB L2.
+Default workload -- BASELINE.json configs[4], the largest configuration and the
+one the multi-GPU target is stated on: DGEMM and ZGEMM 16x16, 10^7 independent
+pairs each, N/N, general alpha and beta, packed layout ("finite-element
+element-matrix scale"), split over the GPUs (strong scaling).  One step = one
+pass of the whole hot path over the rank's pairs: one d16 call and one z16 call.
+The d16 operands occupy the first half of the z16 operand buffers (184 GB of
+separate buffers would not fit in one B200's HBM); both are far larger than L2.
+
+Sub-records on the same line (one GPU only):
+  * "cfg2"  -- configs[1], the paper's headline K20c workload (SGEMM 100,000 pairs
+    at n = 10 and 16, general alpha/beta), as round 1 timed it;
+  * "gate"  -- the north-star target: every type x n = 1..16 x every op pair x
+    {beta == 0, general} at 10^6 pairs, fraction of the measured HBM peak,
+    sustained over rotating buffer sets of >= 4 x L2, CUDA-graph-timed;
+  * "selfcheck" -- inside the cpu_baseline leg: the timed kernels' outputs on
+    sampled pairs against the oracle (the only oracle use besides --impl reference).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--workload cfg5|cfg2|cfg1] [--no-gate] [--no-e2e] [--no-cpu]
 
-Under torchrun each rank owns its own 100,000-pair batches (weak scaling, no
-data-path collective); the time is the max over ranks.  Prints ONE JSON line on
-rank 0.  `value` is GFlop/s by the paper's convention (2n^3 per pair,
-PAPER.md:567-570) over all ranks; GB/s and the roofline are reported beside it.
+--gpus N without torchrun in the environment relaunches itself under
+torch.distributed.run with N ranks (gloo when fewer GPUs than ranks are visible).
+Prints ONE JSON line on rank 0.  `value` is GFlop/s by the paper's convention
+(2n^3 per real pair, 8n^3 per complex pair) over all ranks.
 """
 from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -28,51 +42,33 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+METRIC = "batched GEMM GFlop/s and HBM GB/s (% of peak) vs size n=1..16, 1-8 B200"
+L2_BYTES = 126 * 1024 * 1024
 WORKLOADS = {
-    # BASELINE.json configs[1]: the paper's headline K20c workload (the default)
-    "cfg2": dict(kind="s", sizes=(10, 16), batch=100_000, beta0=False, sets=2, scaling="weak",
-                 text="cfg2: SGEMM 100,000 independent pairs at n=10 and at n=16, op N/N, general "
-                      "alpha/beta, packed (minimal leading dimensions)",
+    # BASELINE.json configs[4] (the default)
+    "cfg5": dict(calls=(("d", 16), ("z", 16)), batch=10_000_000, beta0=False, sets=1,
+                 scaling="strong", shared_dz=True,
+                 text="configs[4]: DGEMM and ZGEMM 16x16, 10^7 independent pairs each (split over "
+                      "the GPUs), op N/N, general alpha/beta, packed (minimal leading dimensions)",
+                 l2="operands 61 GB (d) / 123 GB (z) per GPU at N=1, >> 126 MB L2"),
+    # configs[1]: the paper's headline K20c workload
+    "cfg2": dict(calls=(("s", 10), ("s", 16)), batch=100_000, beta0=False, sets=2,
+                 scaling="weak", shared_dz=False,
+                 text="configs[1]: SGEMM 100,000 independent pairs at n=10 and at n=16, op N/N, "
+                      "general alpha/beta, packed (minimal leading dimensions)",
                  l2="2 alternating input sets of 570 MB (> 126 MB L2)"),
-    # configs[0]: small case (latency-bound; reported in us per step)
-    "cfg1": dict(kind="s", sizes=(4,), batch=1_000, beta0=True, sets=1, scaling="weak",
-                 text="cfg1: SGEMM 1,000 pairs of 4x4, N/N, alpha=1, beta=0",
+    # configs[0]: the small case (latency-bound)
+    "cfg1": dict(calls=(("s", 4),), batch=1_000, beta0=True, sets=1, scaling="weak",
+                 shared_dz=False, text="configs[0]: SGEMM 1,000 pairs of 4x4, N/N, alpha=1, beta=0",
                  l2="192 KB working set: L2-resident by construction (latency-bound case)"),
-    # configs[4]: D/Z 16x16, 10^7 pairs sharded over the GPUs (strong scaling)
-    "cfg5d": dict(kind="d", sizes=(16,), batch=10_000_000, beta0=False, sets=1, scaling="strong",
-                  text="cfg5: DGEMM 16x16, 10^7 pairs in total split over the GPUs, general alpha/beta",
-                  l2="inputs 61 GB >> 126 MB L2"),
-    "cfg5z": dict(kind="z", sizes=(16,), batch=10_000_000, beta0=False, sets=1, scaling="strong",
-                  text="cfg5: ZGEMM 16x16, 10^7 pairs in total split over the GPUs, general alpha/beta",
-                  l2="inputs 123 GB >> 126 MB L2"),
 }
-KIND, SIZES, BATCH, GLOBAL_BATCH, BETA0, NSETS, SCALING = "s", (10, 16), 100_000, 100_000, False, 2, "weak"
-RANGE = (0, 100_000)
-WORKLOAD, L2NOTE = WORKLOADS["cfg2"]["text"], WORKLOADS["cfg2"]["l2"]
 TYPENAME = {"s": "float", "d": "double", "c": "float2", "z": "double2"}
 DTYPE = {"s": "f32", "d": "f64", "c": "c64 (f32 pairs)", "z": "c128 (f64 pairs)"}
-
-
-def configure(name, world, rank):
-    """Select the workload; per-rank pair range (weak: fixed per rank, strong: split)."""
-    global KIND, SIZES, BATCH, GLOBAL_BATCH, BETA0, NSETS, SCALING, RANGE, WORKLOAD, L2NOTE
-    from paper_1304_7053_b200 import shard
-
-    w = WORKLOADS[name]
-    KIND, SIZES, BETA0, NSETS, SCALING = w["kind"], w["sizes"], w["beta0"], w["sets"], w["scaling"]
-    WORKLOAD, L2NOTE = w["text"], w["l2"]
-    if SCALING == "weak":
-        RANGE = shard.weak_range(w["batch"], rank)
-        GLOBAL_BATCH = w["batch"] * world
-    else:
-        RANGE = shard.strong_range(w["batch"], world, rank)
-        GLOBAL_BATCH = w["batch"]
-    BATCH = RANGE[1] - RANGE[0]
-METRIC = "batched GEMM GFlop/s and HBM GB/s (% of peak) vs size n=1..16, 1-8 B200"
 PAPER_CONTEXT = {"hw": "Tesla K20c", "alpha1_beta0_gflops": {"10": 104, "16": 216},
                  "cite": "PAPER.md:37-38, 757, 763 (Table 1)"}
 
 
+# ------------------------------------------------------------------ helpers
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -82,14 +78,24 @@ def peaks():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic():
-    """dram bytes per launch of the dominant kernel from the committed ncu capture."""
+def ncu_traffic(kernel_key):
+    """DRAM bytes per PAIR of a kernel from the committed ncu capture (profiles/)."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
             d = json.load(f)
-        return d.get("bench_dominant_kernel", {}).get("dram_bytes_per_launch")
+        e = d.get("traffic_per_pair", {}).get(kernel_key)
+        return (e["dram_bytes_per_pair"], e["source"]) if e else (None, None)
     except Exception:
-        return None
+        return None, None
+
+
+def scalars(kind, beta0):
+    import txinputs
+
+    a = txinputs.scalar(kind, txinputs.stream_key(txinputs.DEFAULT_SEED, "bench", "alpha", kind))
+    if beta0:
+        return (1.0, 0.0)
+    return a, txinputs.scalar(kind, txinputs.stream_key(txinputs.DEFAULT_SEED, "bench", "beta", kind))
 
 
 class ClockSampler:
@@ -133,87 +139,463 @@ class ClockSampler:
             if len(parts) < 7:
                 continue
             try:
-                rows.append((ts, float(parts[0]), float(parts[1]), parts[3:7]))
+                rows.append((ts, float(parts[0]), float(parts[1]), float(parts[2]), parts[3:7]))
             except ValueError:
                 continue
         inside = [r for r in rows if t0 - 0.05 <= r[0] <= t1 + 0.05] or rows[-3:]
         if not inside:
             return None
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in inside for i, v in enumerate(r[3])
+        reasons = sorted({names[i] for r in inside for i, v in enumerate(r[4])
                           if v.lower() in ("active", "1", "yes")})
         return {"sm_mhz": statistics.median(r[1] for r in inside),
                 "sm_max_mhz": max(r[2] for r in inside), "reasons": reasons,
-                "samples": len(inside)}
+                "power_w_max": max(r[3] for r in inside), "samples": len(inside)}
+
+
+# --------------------------------------------------------- launcher / dist
+def relaunch_under_torchrun(args):
+    """--gpus N with no torchrun environment: run N ranks of this script."""
+    import torch
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    argv = [a for a in sys.argv[1:]]
+    if torch.cuda.device_count() < args.gpus and "--dist-backend" not in argv:
+        argv += ["--dist-backend", "gloo"]  # several ranks per GPU: NCCL refuses that
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1", "--master-port",
+           str(port), os.path.abspath(__file__)] + argv
+    return subprocess.call(cmd)
 
 
 def dist_setup(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}: launch with "
+                         f"--nproc-per-node {args.gpus} (or without torchrun)")
     if world > 1 and args.impl == "ours":
+        import torch
         import torch.distributed as dist
 
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group(args.dist_backend)
+        backend = args.dist_backend
+        if backend == "nccl" and torch.cuda.device_count() < world:
+            backend = "gloo"
+        args.dist_backend = backend
+        dist.init_process_group(backend)
     return world, rank, local
 
 
-def make_inputs(rank, set_id, device):
-    """Seeded synthetic batch for one rank: its global pair range RANGE of the workload."""
-    import txinputs
+def max_over_ranks(v, dev, args):
+    import torch
+
+    t = torch.tensor([v], device=dev if args.dist_backend == "nccl" else "cpu")
+    torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ------------------------------------------------------------ main workload
+def pair_range(wl, world, rank):
     from paper_1304_7053_b200 import shard
 
+    if wl["scaling"] == "weak":
+        return shard.weak_range(wl["batch"], rank), wl["batch"] * world
+    return shard.strong_range(wl["batch"], world, rank), wl["batch"]
+
+
+def fill(dst, kind, key, start, chunk=1 << 25):
+    """dst[i] = txinputs value start + i of stream `key` (generated on the device in
+    chunks, written in place: no full-size temporaries)."""
+    import txinputs
+
+    n = dst.numel()
+    for c0 in range(0, n, chunk):
+        c1 = min(n, c0 + chunk)
+        dst[c0:c1] = txinputs.values_torch(kind, key, start + c0, c1 - c0, dst.device)
+
+
+def make_operands(wl, rng, device, set_id):
+    """{call index: (A, B, C)} packed operands of the rank's pairs [lo, hi)."""
+    import torch
+
+    import txinputs
+
+    lo, hi = rng
+    P = hi - lo
+    key = lambda kind, n, nm: txinputs.stream_key(txinputs.DEFAULT_SEED, "bench", set_id, kind, n,
+                                                  nm)
     out = {}
-    for n in SIZES:
-        key = lambda name: txinputs.stream_key(txinputs.DEFAULT_SEED, "bench", set_id, KIND, n, name)
-        lo, hi = shard.element_range(RANGE, n * n)
-        out[n] = tuple(txinputs.values_torch(KIND, key(nm), lo, hi - lo, device)
+    if wl["shared_dz"]:  # d16 operands = first half of the z16 operand buffers
+        (kd, nd), (kz, nz) = wl["calls"]
+        e = nz * nz
+        for nm in ("A", "B", "C"):
+            Z = torch.empty(P * e, dtype=torch.complex128, device=device)
+            D = Z.view(torch.float64)[: P * e]
+            fill(D, "d", key("d", nd, nm), lo * e)
+            fill(Z[P * e // 2:], "z", key("z", nz, nm), lo * e + P * e // 2)
+            out.setdefault(0, []).append(D)
+            out.setdefault(1, []).append(Z)
+        return {i: tuple(v) for i, v in out.items()}
+    for i, (kind, n) in enumerate(wl["calls"]):
+        e = n * n
+        out[i] = tuple(txinputs.values_torch(kind, key(kind, n, nm), lo * e, P * e, device)
                        for nm in ("A", "B", "C"))
     return out
 
 
-def scalars():
-    import txinputs
+class Runner:
+    """The library calls of one step on resident operands."""
 
-    ka = txinputs.stream_key(txinputs.DEFAULT_SEED, "bench", "alpha")
-    kb = txinputs.stream_key(txinputs.DEFAULT_SEED, "bench", "beta")
-    if BETA0:
-        return 1.0, 0.0
-    return txinputs.scalar(KIND, ka), txinputs.scalar(KIND, kb)
+    def __init__(self, wl, P, stream):
+        import paper_1304_7053_b200 as tx
+
+        self.tx, self.wl, self.P, self.stream = tx, wl, P, stream
+        self.ab = [scalars(kind, wl["beta0"]) for kind, _ in wl["calls"]]
+        self.launches = 0
+
+    def call(self, i, ops):
+        kind, n = self.wl["calls"][i]
+        A, B, C = ops
+        alpha, beta = self.ab[i]
+        rc = self.tx.tx_gemm_batched(kind, "N", "N", n, n, n, alpha, A, n, n * n, B, n, n * n,
+                                     beta, C, n, n * n, self.P, self.stream)
+        if rc != 0:
+            raise self.tx.TxError(rc, self.tx.status_string(rc))
+        self.launches += self.tx.last_path()[1]
+
+    def step(self, sets, s):
+        for i in range(len(self.wl["calls"])):
+            self.call(i, sets[s % len(sets)][i])
 
 
-def cpu_oracle_rate(seconds_budget=12.0, pairs=4000):
-    """The oracle as it stands (single-threaded C loop), run by T host threads on
-    contiguous sub-batches of a bounded sample of the workload; GFlop/s."""
-    import numpy as np
+def call_bytes(kind, n, P, beta0):
+    from paper_1304_7053_b200 import model
 
-    import oracle
+    return model.bytes_moved(kind, n, n, n, P, True, not beta0)
+
+
+def time_workload(wl, rng, world, dev, args, local, with_clocks=True):
+    """Warm-up, the timed region (K steps), per-launch rooflines, evented shares."""
+    import torch
+
+    from paper_1304_7053_b200 import model
+
+    P = rng[1] - rng[0]
+    sets = [make_operands(wl, rng, dev, s) for s in range(wl["sets"])]
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    run = Runner(wl, P, stream)
+    K, W = args.steps, args.warmup
+    for i in range(W):
+        run.step(sets, i)
+    run.launches = 0
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    clk = ClockSampler(local) if with_clocks else None
+    if clk:
+        clk.start()
+        time.sleep(0.2)  # let the sampler attach before the timed region
+    # ---- timed region: K steps, events only at the two ends (launch overlap kept)
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t_wall0 = time.time()
+    start.record(stream)
+    for i in range(K):
+        run.step(sets, i)
+    end.record(stream)
+    torch.cuda.synchronize()
+    t_wall1 = time.time()
+    ms = start.elapsed_time(end)
+    launches = run.launches
+    clocks = clk.stop(t_wall0, t_wall1) if clk else None
+    if world > 1:
+        torch.distributed.barrier()
+        ms = max_over_ranks(ms, dev, args)
+    # ---- per-kernel rooflines: R back-to-back launches of one call alone
+    per_launch = {}
+    for i, (kind, n) in enumerate(wl["calls"]):
+        est_ms = call_bytes(kind, n, P, wl["beta0"]) / 6.5e9
+        R = int(max(10, min(200, 300.0 / max(est_ms, 1e-3))))
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for r in range(R):
+            run.call(i, sets[r % len(sets)][i])
+        b.record(stream)
+        torch.cuda.synchronize()
+        per_launch[i] = (a.elapsed_time(b) / R, R)
+    # ---- per-launch events (each launch bracketed): each kernel's share of the step
+    evs = []
+    for s in range(min(K, 10)):
+        for i in range(len(wl["calls"])):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            run.call(i, sets[s % len(sets)][i])
+            b.record(stream)
+            evs.append((i, a, b))
+    torch.cuda.synchronize()
+    evented = {i: statistics.mean(a.elapsed_time(b) for j, a, b in evs if j == i)
+               for i in range(len(wl["calls"]))}
+    flops_step = sum(model.flops(kind, n, n, n, P) for kind, n in wl["calls"])
+    bytes_step = sum(call_bytes(kind, n, P, wl["beta0"]) for kind, n in wl["calls"])
+    return dict(sets=sets, run=run, ms=ms, launches=launches, clocks=clocks, per_launch=per_launch,
+                evented=evented, flops_step=flops_step, bytes_step=bytes_step, P=P)
+
+
+def roofline_of(wl, res, peak, peak_src):
+    """Roofline of the dominant kernel (largest algorithmic bytes per launch)."""
+    P = res["P"]
+    by = {i: call_bytes(kind, n, P, wl["beta0"]) for i, (kind, n) in enumerate(wl["calls"])}
+    dom = max(by, key=by.get)
+    kind, n = wl["calls"][dom]
+    ms, R = res["per_launch"][dom]
+    achieved = by[dom] / (ms / 1e3) / 1e9
+    tkey = f"{kind}{n}_NN_{'b0' if wl['beta0'] else 'general'}"
+    tpp, tsrc = ncu_traffic(tkey)
+    return {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+            "frac": round(achieved / peak, 4),
+            "traffic": round(tpp * P) if tpp else None,
+            "traffic_source": tsrc,
+            "kernel": f"bulk_kernel<{TYPENAME[kind]},{n},{n},{n},N,N,beta{'==' if wl['beta0'] else '!='}0>",
+            "algorithmic_bytes_per_launch": by[dom],
+            "algorithmic_bytes_per_pair": by[dom] // P,
+            "launch_ms": round(ms, 5),
+            "launch_ms_evented": round(res["evented"][dom], 5),
+            "share_of_step_evented": round(res["evented"][dom] / sum(res["evented"].values()), 4),
+            "timing": f"{R} back-to-back launches, CUDA events at both ends on the launch stream",
+            "peak_source": peak_src,
+            "per_call_gbps": {f"{k}{nn}": round(by[i] / (res["per_launch"][i][0] / 1e3) / 1e9, 1)
+                              for i, (k, nn) in enumerate(wl["calls"])},
+            "per_call_frac": {f"{k}{nn}": round(by[i] / (res["per_launch"][i][0] / 1e3) / 1e9
+                                                 / peak, 4)
+                              for i, (k, nn) in enumerate(wl["calls"])}}
+
+
+# ------------------------------------------------------------------- e2e
+def e2e_of(wl, res, world, dev, args):
+    """Same metric end to end through tx_gemm_batched_hostio_<t>: pinned host
+    buffers, host->device and device->host copies inside the timed region."""
+    import torch
+
+    import paper_1304_7053_b200 as tx
+    from paper_1304_7053_b200 import model
+
+    P = res["P"]
+    EB = min(P, 100_000)
+    ops = res["sets"][0]
+    host, staging = {}, {}
+    for i, (kind, n) in enumerate(wl["calls"]):
+        e = n * n
+        host[i] = tuple(x[: EB * e].cpu().pin_memory() for x in ops[i])
+        staging[i] = tuple(x[: EB * e] for x in ops[i])  # device staging: the resident buffers
+    h2d = sum(x.numel() * x.element_size() for i in host for x in host[i])
+    d2h = sum(host[i][2].numel() * host[i][2].element_size() for i in host)
+    stream = torch.cuda.current_stream()
+    run = res["run"]
+
+    def e2e_step():
+        for i, (kind, n) in enumerate(wl["calls"]):
+            hA, hB, hC = host[i]
+            dA, dB, dC = staging[i]
+            alpha, beta = run.ab[i]
+            rc = tx.tx_gemm_batched_hostio(kind, "N", "N", n, n, n, alpha, hA, n, n * n, hB, n,
+                                           n * n, beta, hC, n, n * n, EB, stream, dA, dB, dC)
+            if rc != 0:
+                raise tx.TxError(rc, tx.status_string(rc))
+
+    KE = max(1, min(args.steps, 10))
+    for _ in range(min(args.warmup, 2)):
+        e2e_step()
+    torch.cuda.synchronize()
+    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s0.record(stream)
+    for _ in range(KE):
+        e2e_step()
+    s1.record(stream)
+    torch.cuda.synchronize()
+    ems = s0.elapsed_time(s1)
+    if world > 1:
+        ems = max_over_ranks(ems, dev, args)
+    flops_e2e = sum(model.flops(kind, n, n, n, EB) for kind, n in wl["calls"])
+    names = "/".join(f"tx_gemm_batched_hostio_{k}" for k in sorted({k for k, _ in wl["calls"]}))
+    return {"value": round(flops_e2e * KE * world / (ems / 1e3) / 1e9, 2), "unit": "GFlop/s",
+            "pairs_per_call_per_step": EB, "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h, "steps": KE,
+            "api": f"{names} (pinned host buffers, copies inside the timed region)"}
+
+
+# ------------------------------------------------------------ the gate
+def gate_sweep(dev, peak, batch=1_000_000, target_ms=12.0, max_reps=100):
+    """Every type x n = 1..16 x every op pair x {beta == 0, general} at `batch` pairs:
+    algorithmic GB/s as a fraction of the measured HBM peak.  Sustained protocol:
+    rotating buffer sets whose total footprint is >= 4 x L2 (no set is L2-resident
+    when reused); the back-to-back calls are captured once in a CUDA graph and the
+    graph is replayed, so the host's per-call cost does not mask the device time."""
+    import torch
+
+    import paper_1304_7053_b200 as tx
     import txinputs
     from paper_1304_7053_b200 import model
 
-    alpha, beta = scalars()
-    T = len(os.sched_getaffinity(0))
+    pool_bytes = batch * 256 * 16  # one z16 operand at `batch` pairs
+    pools = [torch.empty(pool_bytes, dtype=torch.uint8, device=dev) for _ in range(3)]
+    rdt = {"s": torch.float32, "d": torch.float64, "c": torch.float32, "z": torch.float64}
+    cdt = {"s": torch.float32, "d": torch.float64, "c": torch.complex64, "z": torch.complex128}
+    results = []
+    cap_stream = torch.cuda.Stream()
+    t0 = time.time()
+    for kind in "sdcz":
+        for j, pool in enumerate(pools):
+            fill(pool.view(rdt[kind]), "d" if rdt[kind] == torch.float64 else "s",
+                 txinputs.stream_key(txinputs.DEFAULT_SEED, "gate", kind, j), 0)
+        views = [p.view(cdt[kind]) for p in pools]
+        alpha = txinputs.scalar(kind, txinputs.stream_key(txinputs.DEFAULT_SEED, "gate", "a", kind))
+        betag = txinputs.scalar(kind, txinputs.stream_key(txinputs.DEFAULT_SEED, "gate", "b", kind))
+        ops = "NTC" if kind in "cz" else "NT"
+        es = model.ESIZE[kind]
+        for n in range(1, 17):
+            e = n * n
+            per_op = batch * e * es
+            sets = max(1, min(pool_bytes // per_op, math.ceil(4 * L2_BYTES / (3 * per_op))))
+            for ta in ops:
+                for tb in ops:
+                    for beta0 in (True, False):
+                        beta = 0 if beta0 else betag
+                        byts = model.bytes_moved(kind, n, n, n, batch, True, not beta0)
+                        reps = int(max(4, min(max_reps, target_ms / (byts / (peak * 1e6)))))
+
+                        def call(r):
+                            s = r % sets
+                            A = views[0][s * batch * e:(s + 1) * batch * e]
+                            B = views[1][s * batch * e:(s + 1) * batch * e]
+                            C = views[2][s * batch * e:(s + 1) * batch * e]
+                            rc = tx.tx_gemm_batched(kind, ta, tb, n, n, n, alpha, A, n, e, B, n, e,
+                                                    beta, C, n, e, batch)
+                            assert rc == 0, tx.status_string(rc)
+
+                        with torch.cuda.stream(cap_stream):
+                            call(0)  # warm: occupancy caches, attributes
+                            g = torch.cuda.CUDAGraph()
+                            with torch.cuda.graph(g, stream=cap_stream):
+                                for r in range(reps):
+                                    call(r)
+                            g.replay()
+                            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                            a.record(cap_stream)
+                            g.replay()
+                            b.record(cap_stream)
+                        torch.cuda.synchronize()
+                        ms = a.elapsed_time(b) / reps
+                        del g
+                        results.append({"kind": kind, "n": n, "ops": ta + tb, "beta0": beta0,
+                                        "us": round(ms * 1e3, 3),
+                                        "frac": round(byts / (ms / 1e3) / 1e9 / peak, 4),
+                                        "sets": sets, "reps": reps})
+    wall = time.time() - t0
+    del pools, views
+    torch.cuda.empty_cache()
+    return results, wall
+
+
+def gate_summary(results, batch, wall):
+    fr = [r["frac"] for r in results]
+    big = [r for r in results if r["n"] >= 3]
+    tiny = [r for r in results if r["n"] <= 2]
     per = {}
-    for n in SIZES:
-        key = lambda name: txinputs.stream_key(txinputs.DEFAULT_SEED, "bench", 0, KIND, n, name)
+    for r in results:
+        per.setdefault(f"{r['kind']}{r['n']}", []).append(r)
+    compact = {}
+    for key, rs in per.items():
+        w = min(rs, key=lambda r: r["frac"])
+        nn = {("b0" if r["beta0"] else "gen"): r["frac"] for r in rs if r["ops"] == "NN"}
+        compact[key] = {"NN_b0": nn.get("b0"), "NN_gen": nn.get("gen"),
+                        "min": w["frac"], "min_at": w["ops"] + ("/b0" if w["beta0"] else "/gen"),
+                        "median": round(statistics.median(r["frac"] for r in rs), 4)}
+    return {"batch_pairs": batch, "instances": len(results),
+            "frac_of": "measured HBM peak (MEASURED_PEAKS.json hbm_gbs)",
+            "timing": "CUDA graph of back-to-back calls over rotating sets >= 4 x L2, replayed",
+            "target": ">= 0.70 of HBM at 10^6 pairs for every (type, op, n <= 16) (north_star); "
+                      "0.855 of measured = 0.70 of the nominal 8 TB/s",
+            "summary": {"min_all": min(fr), "median_all": round(statistics.median(fr), 4),
+                        "min_n_ge_3": min(r["frac"] for r in big),
+                        "min_n_le_2": min(r["frac"] for r in tiny),
+                        "n_ge_0.70": sum(f >= 0.70 for f in fr),
+                        "n_ge_0.855": sum(f >= 0.855 for f in fr),
+                        "n_ge_3_ge_0.855": sum(r["frac"] >= 0.855 for r in big),
+                        "n_ge_3": len(big)},
+            "per_type_n": compact, "wall_s": round(wall, 1)}
+
+
+# --------------------------------------------------- cpu baseline + selfcheck
+def cpu_baseline_and_selfcheck(wl, res, seconds_budget=12.0, samples=4096):
+    """The oracle as it stands (single-threaded C loop) on T host threads over a
+    bounded sample of the workload -- the sampled pairs of the timed kernels' own
+    outputs.  The same oracle results check those outputs element by element
+    (north-star tolerance, den = |alpha| sum|op(A)||op(B)| + |beta||C0|)."""
+    import numpy as np
+    import torch
+
+    import oracle
+    from paper_1304_7053_b200 import model
+
+    P = res["P"]
+    run = res["run"]
+    ops = res["sets"][0]
+    rng = np.random.default_rng(12345)
+    idx = np.unique(np.concatenate([[0, P - 1], rng.integers(0, P, samples)]))
+    ti = torch.as_tensor(idx, device=ops[0][0].device)
+    tol = {"s": 1e-5, "c": 1e-5, "d": 1e-13, "z": 1e-13}
+    wide = {"s": np.float64, "d": np.float64, "c": np.complex128, "z": np.complex128}
+    check = {}
+    sample = {}
+    # z before d: the d16 operands live inside the z16 buffers, so each call's C
+    # samples are read right before and right after that call alone
+    for i in reversed(range(len(wl["calls"]))):
+        kind, n = wl["calls"][i]
         e = n * n
-        per[n] = [txinputs.values_numpy(KIND, key(nm), 0, pairs * e).copy() for nm in ("A", "B", "C")]
-    flops_one = sum(model.flops(KIND, n, n, n, pairs) for n in SIZES)
+        A, B, C = ops[i]
+        C0 = C.view(-1, e)[ti].cpu().numpy().ravel()
+        hA = A.view(-1, e)[ti].cpu().numpy().ravel()
+        hB = B.view(-1, e)[ti].cpu().numpy().ravel()
+        run.call(i, ops[i])
+        torch.cuda.synchronize()
+        got = C.view(-1, e)[ti].cpu().numpy().ravel()
+        alpha, beta = run.ab[i]
+        s = len(idx)
+        ref = C0.copy()
+        assert oracle.gemm_batched(kind, "N", "N", n, n, n, alpha, hA, n, e, hB, n, e, beta, ref,
+                                   n, e, s) == 0
+        Ad = hA.reshape(s, n, n).transpose(0, 2, 1).astype(wide[kind])
+        Bd = hB.reshape(s, n, n).transpose(0, 2, 1).astype(wide[kind])
+        den = abs(alpha) * np.einsum("pil,plj->pij", np.abs(Ad), np.abs(Bd))
+        if beta != 0:
+            den = den + abs(beta) * np.abs(C0.reshape(s, n, n).transpose(0, 2, 1))
+        diff = np.abs(got.astype(wide[kind]) - ref.astype(wide[kind])).reshape(s, n, n)
+        err = float(np.max(diff.transpose(0, 2, 1) / np.maximum(den, np.finfo(np.float64).tiny)))
+        check[f"{kind}{n}"] = {"pairs": s, "max_rel_err": err, "tol": tol[kind],
+                               "ok": bool(err <= tol[kind])}
+        sample[i] = (hA, hB, C0)
+    # ---- the oracle's rate on T threads over the same sample
+    T = len(os.sched_getaffinity(0))
+    flops_one = sum(model.flops(kind, n, n, n, len(idx)) for kind, n in wl["calls"])
 
     def work(tid, reps, out):
         t = 0.0
         for _ in range(reps):
-            for n in SIZES:
-                A, B, C = per[n]
-                Cw = C.copy()
+            for i, (kind, n) in enumerate(wl["calls"]):
+                hA, hB, C0 = sample[i]
+                Cw = C0.copy()
+                alpha, beta = run.ab[i]
                 t0 = time.perf_counter()
-                oracle.gemm_batched(KIND, "N", "N", n, n, n, alpha, A, n, n * n, B, n, n * n, beta,
-                                    Cw, n, n * n, pairs)
+                oracle.gemm_batched(kind, "N", "N", n, n, n, alpha, hA, n, n * n, hB, n, n * n,
+                                    beta, Cw, n, n * n, len(idx))
                 t += time.perf_counter() - t0
         out[tid] = t
 
-    # calibrate on one thread, then size the multi-threaded run to the budget
     o = {}
     work(0, 1, o)
     t1 = max(o[0], 1e-6)
@@ -226,43 +608,124 @@ def cpu_oracle_rate(seconds_budget=12.0, pairs=4000):
     for th in ths:
         th.join()
     wall = time.perf_counter() - t0
-    total = flops_one * reps * T
-    return {"value": round(total / wall / 1e9, 3), "unit": "GFlop/s", "cores": T, "kind": "oracle",
-            "sample": f"{reps} x {pairs} pairs per size (n=10 and n=16) per thread on {T} "
-                      f"threads, each thread running the unchanged single-threaded oracle",
-            "single_thread_gflops": round(flops_one / t1 / 1e9, 3)}
+    calls = "+".join(f"{k}{n}" for k, n in wl["calls"])
+    cpu = {"value": round(flops_one * reps * T / wall / 1e9, 3), "unit": "GFlop/s", "cores": T,
+           "kind": "oracle",
+           "sample": f"{len(idx)} sampled pairs of each call ({calls}) of the timed workload, "
+                     f"{reps} repetitions per thread on {T} threads, each thread running the "
+                     f"unchanged single-threaded oracle",
+           "single_thread_gflops": round(flops_one / t1 / 1e9, 3)}
+    selfcheck = {"pairs_per_call": len(idx), "calls": check,
+                 "ok": all(c["ok"] for c in check.values()),
+                 "how": "one extra step after the timed region; C sampled before and after each "
+                        "call; the oracle recomputes the sampled pairs"}
+    return cpu, selfcheck
 
 
-def run_reference(args, world, rank):
-    """--impl reference: the oracle, as it stands, on the host cores; each step a
-    bounded sample of the workload."""
-    if rank != 0:
-        return
-    import oracle  # noqa: F401
+# ----------------------------------------------------------------- our arm
+def run_ours(args, world, rank, local):
+    import torch
+
+    import paper_1304_7053_b200 as tx
     from paper_1304_7053_b200 import model
 
-    pairs = 2000
-    T = len(os.sched_getaffinity(0))
+    local = local % max(1, torch.cuda.device_count())  # several ranks per GPU only when testing
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    tx.lib()  # fails loudly if the CUDA library is missing: no fallback
+    peak, peak_src = peaks()
+    wl = WORKLOADS[args.workload]
+    rng, global_batch = pair_range(wl, world, rank)
+    res = time_workload(wl, rng, world, dev, args, local)
+    K, ms = args.steps, res["ms"]
+    # work of ALL ranks per step (the global pairs of every call) / max-over-ranks time
+    total_flops = sum(model.flops(k, n, n, n, global_batch) for k, n in wl["calls"])
+    total_bytes = sum(call_bytes(k, n, global_batch, wl["beta0"]) for k, n in wl["calls"])
+    value = total_flops * K / (ms / 1e3) / 1e9
+    gbps = total_bytes * K / (ms / 1e3) / 1e9
+    roofline = roofline_of(wl, res, peak, peak_src)
+    e2e = None if args.no_e2e else e2e_of(wl, res, world, dev, args)
+    cpu = selfcheck = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu, selfcheck = cpu_baseline_and_selfcheck(wl, res)
+    launches = res["launches"]
+    clocks = res["clocks"]
+    sub = {}
+    del res
+    torch.cuda.empty_cache()
+    if world == 1 and args.workload == "cfg5" and not args.no_sub:
+        # configs[1] sub-record (the round-1 headline)
+        w2 = WORKLOADS["cfg2"]
+        r2 = time_workload(w2, pair_range(w2, 1, 0)[0], 1, dev, args, local, with_clocks=False)
+        sub["cfg2"] = {"workload": w2["text"],
+                       "value": round(r2["flops_step"] * K / (r2["ms"] / 1e3) / 1e9, 2),
+                       "unit": "GFlop/s", "ms_per_step": round(r2["ms"] / K, 5),
+                       "gbps": round(r2["bytes_step"] * K / (r2["ms"] / 1e3) / 1e9, 1),
+                       "roofline": roofline_of(w2, r2, peak, peak_src), "l2": w2["l2"]}
+        del r2
+        torch.cuda.empty_cache()
+        if not args.no_gate:
+            results, wall = gate_sweep(dev, peak)
+            sub["gate"] = gate_summary(results, 1_000_000, wall)
+            if args.gate_out:
+                with open(args.gate_out, "w") as f:
+                    for r in results:
+                        f.write(json.dumps(r) + "\n")
+    if rank == 0:
+        calls = "+".join(f"{k}{n}" for k, n in wl["calls"])
+        line = {"metric": METRIC, "value": round(value, 2), "unit": "GFlop/s", "n_gpus": world,
+                "steps": K, "warmup": args.warmup, "ms_per_step": round(ms / K, 5),
+                "higher_is_better": True, "scaling": wl["scaling"], "vs_baseline": None,
+                "dtype": "/".join(DTYPE[k] for k in dict.fromkeys(k for k, _ in wl["calls"])),
+                "data": "synthetic (seeded counter-based U[-1,1), txinputs)",
+                "config": {"workload": wl["text"], "calls_per_step": calls,
+                           "pairs_per_call_per_gpu": rng[1] - rng[0],
+                           "global_pairs_per_call": global_batch,
+                           "parallelism": f"dp{world} (independent pairs, no collective)"
+                                          + (" [gloo, ranks share GPUs]"
+                                             if args.dist_backend == "gloo" and world > 1 else ""),
+                           "l2": wl["l2"]},
+                "gbps": round(gbps, 1), "hbm_frac": round(gbps / world / peak, 4),
+                "roofline": roofline, "cpu_baseline": cpu, "selfcheck": selfcheck, "e2e": e2e,
+                "gpu_launches": launches, "clocks": clocks, **sub,
+                "paper_context": PAPER_CONTEXT}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.barrier()
+        torch.distributed.destroy_process_group()
+
+
+# ----------------------------------------------------------- reference arm
+def run_reference(args, world, rank):
+    """--impl reference: the oracle, as it stands, on the host cores; each step a
+    bounded sample of the workload (pairs_per_thread pairs of each call per thread)."""
+    if rank != 0:
+        return
     import numpy as np
 
+    import oracle
     import txinputs
+    from paper_1304_7053_b200 import model
 
-    alpha, beta = scalars()
+    wl = WORKLOADS[args.workload]
+    pairs = 2048
+    T = len(os.sched_getaffinity(0))
     data = {}
-    for n in SIZES:
-        key = lambda name: txinputs.stream_key(txinputs.DEFAULT_SEED, "bench", 0, KIND, n, name)
+    for i, (kind, n) in enumerate(wl["calls"]):
+        key = lambda nm: txinputs.stream_key(txinputs.DEFAULT_SEED, "bench", 0, kind, n, nm)
         e = n * n
-        data[n] = [txinputs.values_numpy(KIND, key(nm), 0, pairs * T * e).copy()
+        data[i] = [txinputs.values_numpy(kind, key(nm), 0, pairs * T * e).copy()
                    for nm in ("A", "B", "C")]
+    ab = [scalars(kind, wl["beta0"]) for kind, _ in wl["calls"]]
 
     def step():
         def w(t):
-            for n in SIZES:
-                A, B, C = data[n]
+            for i, (kind, n) in enumerate(wl["calls"]):
+                A, B, C = data[i]
                 e = n * n
                 sl = slice(t * pairs * e, (t + 1) * pairs * e)
-                oracle.gemm_batched(KIND, "N", "N", n, n, n, alpha, A[sl], n, e, B[sl], n, e, beta,
-                                    C[sl].copy(), n, e, pairs)
+                oracle.gemm_batched(kind, "N", "N", n, n, n, ab[i][0], A[sl], n, e, B[sl], n, e,
+                                    ab[i][1], C[sl].copy(), n, e, pairs)
         ths = [threading.Thread(target=w, args=(t,)) for t in range(T)]
         for th in ths:
             th.start()
@@ -275,210 +738,48 @@ def run_reference(args, world, rank):
     for _ in range(args.steps):
         step()
     dt = time.perf_counter() - t0
-    flops = sum(model.flops(KIND, n, n, n, pairs * T) for n in SIZES) * args.steps
-    byts = sum(model.bytes_moved(KIND, n, n, n, pairs * T, True, not BETA0) for n in SIZES) * args.steps
+    flops = sum(model.flops(k, n, n, n, pairs * T) for k, n in wl["calls"]) * args.steps
+    byts = sum(call_bytes(k, n, pairs * T, wl["beta0"]) for k, n in wl["calls"]) * args.steps
     val = flops / dt / 1e9
+    calls = "+".join(f"{k}{n}" for k, n in wl["calls"])
     line = {"impl": "reference", "metric": METRIC, "value": round(val, 3), "unit": "GFlop/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(dt / args.steps * 1e3, 3), "higher_is_better": True,
-            "scaling": SCALING, "vs_baseline": None, "dtype": DTYPE[KIND], "data": "synthetic",
-            "gbps": round(byts / dt / 1e9, 3),
-            "config": {"workload": WORKLOAD, "kind": KIND, "sizes": list(SIZES), "batch": GLOBAL_BATCH,
-                       "reference_sample": f"{pairs * T} pairs per size per step"},
+            "scaling": wl["scaling"], "vs_baseline": None,
+            "dtype": "/".join(DTYPE[k] for k in dict.fromkeys(k for k, _ in wl["calls"])),
+            "data": "synthetic", "gbps": round(byts / dt / 1e9, 3),
+            "config": {"workload": wl["text"], "calls_per_step": calls,
+                       "reference_sample": f"{pairs * T} pairs of each call per step"},
             "cpu_baseline": {"value": round(val, 3), "unit": "GFlop/s", "cores": T,
                              "kind": "oracle",
-                             "sample": f"{pairs} pairs per size per thread per step, {T} threads"},
+                             "sample": f"{pairs} pairs of each call per thread per step, {T} threads"},
             "e2e": {"value": round(val, 3), "unit": "GFlop/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
-def max_over_ranks(v, dev, args):
-    import torch
-
-    t = torch.tensor([v], device=dev if args.dist_backend == "nccl" else "cpu")
-    torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-    return float(t.item())
-
-
-def run_ours(args, world, rank, local):
-    import torch
-
-    import paper_1304_7053_b200 as tx
-    from paper_1304_7053_b200 import model
-
-    local = local % torch.cuda.device_count()  # several ranks per GPU only when testing (gloo)
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    tx.lib()  # fails loudly if the CUDA library is missing: no fallback
-    alpha, beta = scalars()
-    sets = [make_inputs(rank, s, dev) for s in range(NSETS)]
-    torch.cuda.synchronize()
-    stream = torch.cuda.current_stream()
-    n_launch = [0]
-
-    def call(n, A, B, C):
-        rc = tx.tx_gemm_batched(KIND, "N", "N", n, n, n, alpha, A, n, n * n, B, n, n * n, beta, C,
-                                n, n * n, BATCH, stream)
-        if rc != 0:
-            raise tx.TxError(rc, tx.status_string(rc))
-        n_launch[0] += tx.last_path()[1]
-
-    K, W = args.steps, args.warmup
-
-    def step(i):
-        s = sets[i % NSETS]
-        for n in SIZES:
-            call(n, *s[n])
-
-    for i in range(W):
-        step(i)
-    n_launch[0] = 0
-    if world > 1:
-        torch.distributed.barrier()
-    torch.cuda.synchronize()
-    clk = ClockSampler(local)
-    clk.start()
-    time.sleep(0.2)  # let the sampler attach before the timed region
-    # ---- timed region: K steps, events only at the two ends, so consecutive
-    # launches keep their programmatic-dependent-launch overlap
-    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    t_wall0 = time.time()
-    start.record(stream)
-    for i in range(K):
-        step(i)
-    end.record(stream)
-    torch.cuda.synchronize()
-    t_wall1 = time.time()
-    ms = start.elapsed_time(end)
-    launches = n_launch[0]
-    # ---- roofline of each kernel: R back-to-back launches of that size alone
-    # (alternating input sets), CUDA events on the launch stream at both ends
-    R = max(20, min(K, 200))
-    per_launch = {}
-    for n in SIZES:
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        for i in range(R):
-            call(n, *sets[i % NSETS][n])
-        b.record(stream)
-        torch.cuda.synchronize()
-        per_launch[n] = a.elapsed_time(b) / R
-    # ---- per-launch events (each launch bracketed; breaks the launch overlap):
-    # the kernel's share of the step, to compare with the ncu launch list
-    evs = []
-    for i in range(min(K, 50)):
-        s_ = sets[i % NSETS]
-        for n in SIZES:
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(stream)
-            call(n, *s_[n])
-            b.record(stream)
-            evs.append((n, a, b))
-    torch.cuda.synchronize()
-    clocks = clk.stop(t_wall0, t_wall1)
-    evented = {n: statistics.mean(a.elapsed_time(b) for m_, a, b in evs if m_ == n) for n in SIZES}
-    if world > 1:
-        ms = max_over_ranks(ms, dev, args)
-
-    flops_step = sum(model.flops(KIND, n, n, n, BATCH) for n in SIZES)
-    bytes_step = sum(model.bytes_moved(KIND, n, n, n, BATCH, True, not BETA0) for n in SIZES)
-    value = flops_step * K * world / (ms / 1e3) / 1e9
-    gbps = bytes_step * K * world / (ms / 1e3) / 1e9
-    dom = max(SIZES)
-    dom_bytes = model.bytes_moved(KIND, dom, dom, dom, BATCH, True, not BETA0)
-    peak, peak_src = peaks()
-    achieved = dom_bytes / (per_launch[dom] / 1e3) / 1e9
-    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                "frac": round(achieved / peak, 4), "traffic": ncu_traffic(),
-                "kernel": f"bulk_kernel<{TYPENAME[KIND]},{dom},{dom},{dom},N,N,beta{'==' if BETA0 else '!='}0>",
-                "algorithmic_bytes_per_launch": dom_bytes,
-                "launch_ms": round(per_launch[dom], 5),
-                "launch_ms_evented": round(evented[dom], 5),
-                "share_of_step_evented": round(evented[dom] / sum(evented.values()), 4),
-                "timing": f"{R} back-to-back launches, CUDA events at both ends",
-                "peak_source": peak_src,
-                "per_size_gbps": {str(n): round(model.bytes_moved(KIND, n, n, n, BATCH, True, not BETA0)
-                                                / (per_launch[n] / 1e3) / 1e9, 1) for n in SIZES}}
-
-    # ---- end to end through the host-buffer C-ABI entry (pinned host memory) ----
-    e2e = None
-    if not args.no_e2e:
-        # end to end over at most 2*10^5 pairs of the rank's batch (pinned host memory)
-        EB = min(BATCH, 200_000)
-        host = {n: tuple(x[: EB * n * n].cpu().pin_memory() for x in sets[0][n]) for n in SIZES}
-        staging = {n: tuple(torch.empty_like(x, device=dev) for x in host[n]) for n in SIZES}
-        h2d = sum((x.numel() * x.element_size()) for n in SIZES for x in host[n])
-        d2h = sum(host[n][2].numel() * host[n][2].element_size() for n in SIZES)
-
-        def e2e_step():
-            for n in SIZES:
-                hA, hB, hC = host[n]
-                dA, dB, dC = staging[n]
-                rc = tx.tx_gemm_batched_hostio(KIND, "N", "N", n, n, n, alpha, hA, n, n * n, hB, n,
-                                               n * n, beta, hC, n, n * n, EB, stream, dA, dB, dC)
-                if rc != 0:
-                    raise tx.TxError(rc, tx.status_string(rc))
-
-        KE = max(1, min(K, 20))
-        for _ in range(min(W, 3)):
-            e2e_step()
-        torch.cuda.synchronize()
-        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        s0.record(stream)
-        for _ in range(KE):
-            e2e_step()
-        s1.record(stream)
-        torch.cuda.synchronize()
-        ems = s0.elapsed_time(s1)
-        if world > 1:
-            ems = max_over_ranks(ems, dev, args)
-        flops_e2e = sum(model.flops(KIND, n, n, n, EB) for n in SIZES)
-        e2e = {"value": round(flops_e2e * KE * world / (ems / 1e3) / 1e9, 2), "unit": "GFlop/s",
-               "pairs_per_size_per_step": EB,
-               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": KE,
-               "api": "tx_gemm_batched_hostio_s (host buffers, copies inside the timed region)"}
-
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
-        cpu = cpu_oracle_rate()
-
-    if rank == 0:
-        line = {"metric": METRIC, "value": round(value, 2), "unit": "GFlop/s", "n_gpus": world,
-                "steps": K, "warmup": W, "ms_per_step": round(ms / K, 5),
-                "higher_is_better": True, "scaling": SCALING, "vs_baseline": None,
-                "dtype": DTYPE[KIND],
-                "data": "synthetic (seeded counter-based U[-1,1), txinputs)",
-                "config": {"workload": WORKLOAD, "kind": KIND, "sizes": list(SIZES),
-                           "batch_per_gpu": BATCH, "global_batch": GLOBAL_BATCH,
-                           "parallelism": f"dp{world} (independent pairs, no collective)",
-                           "l2": L2NOTE},
-                "gbps": round(gbps, 1), "hbm_frac": round(gbps / peak, 4),
-                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-                "gpu_launches": launches, "clocks": clocks, "paper_context": PAPER_CONTEXT}
-        print(json.dumps(line), flush=True)
-    if world > 1:
-        torch.distributed.barrier()
-        torch.distributed.destroy_process_group()
-
-
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
-    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--workload", default="cfg5", choices=sorted(WORKLOADS),
+                    help="cfg5 (default, BASELINE configs[4]), cfg2 (configs[1]), cfg1 (configs[0])")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS),
-                    help="cfg2 (default, BASELINE configs[1]), cfg1 (configs[0]), cfg5d/cfg5z "
-                         "(configs[4], 10^7 pairs split over the GPUs)")
+    ap.add_argument("--no-gate", action="store_true", help="skip the 832-instance gate sweep")
+    ap.add_argument("--no-sub", action="store_true", help="skip the cfg2 and gate sub-records")
+    ap.add_argument("--gate-out", default="", help="write every gate instance (JSON lines)")
     ap.add_argument("--dist-backend", default="nccl", choices=("nccl", "gloo"),
-                    help="process-group backend for the barrier / max-over-ranks (gloo: testing "
-                         "several ranks on one GPU)")
+                    help="process group for the barrier / max-over-ranks (gloo: several ranks "
+                         "per GPU, testing)")
     args = ap.parse_args()
+    if args.warmup < 3:
+        raise SystemExit("bench.py: --warmup must be >= 3")
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch_under_torchrun(args))
     world, rank, local = dist_setup(args)
-    configure(args.workload, world, rank)
     if args.impl == "reference":
         run_reference(args, world, rank)  # rank 0 only; other ranks exit 0
         return

@@ -58,8 +58,14 @@
  *   ldb < max(1, rows of stored B) -11 [-10], ldc < max(1, m) -15 [-13];
  *   batch_count > 1 (strided only): lda2 < 0 -9, ldb2 < 0 -12, ldc2 < ldc*n -16;
  *   batch_count < 0 -17 [-14];
- *   A NULL -7 / B NULL -10 [-9] when alpha != 0, k > 0 and m*n*batch_count > 0;
- *   C NULL -14 [-12] when m*n*batch_count > 0;
+ *   A NULL or misaligned -7 / B -10 [-9] when alpha != 0, k > 0 and
+ *   m*n*batch_count > 0; C NULL or misaligned -14 [-12] when m*n*batch_count > 0.
+ *   "Misaligned" (reading R21): strided A, B, C must be aligned to the
+ *   element size -- 4 (s), 8 (d), 8 (c), 16 (z) bytes, as float, double,
+ *   cuComplex (float2) and cuDoubleComplex (double2) are -- because the kernels
+ *   move whole elements; the pointer ARRAYS must be 8-byte aligned, and every
+ *   pointer they hold must be aligned to the element size (documented
+ *   precondition, not checked: it would need device reads);
  *   strided: C's address range overlapping A's or B's -14 (when A/B are read).
  */
 #ifndef TXGEMM_H
@@ -125,7 +131,7 @@ int tx_gemm_batched_ptr_z(char transa, char transb, int m, int n, int k,
  * GEMMs on `stream`, ordered by events, so both PCIe directions and the kernels
  * overlap; work already queued on `stream` is ordered before the first copy and
  * `stream` is ordered after the last one.  Returns as the strided call; a NULL
- * staging buffer that would be used returns -19/-20/-21. ---- */
+ * or misaligned staging buffer that would be used returns -19/-20/-21. ---- */
 int tx_gemm_batched_hostio_s(char transa, char transb, int m, int n, int k,
                              const float *alpha, const float *hA, int lda, long long lda2,
                              const float *hB, int ldb, long long ldb2, const float *beta,
@@ -200,7 +206,8 @@ const char *tx_status_string(int status);
 int tx_version(void);
 /* Path the calling thread's most recent successful GEMM call took:
  * 0 none/quick return, 1 packed bulk-copy (TMA) kernel, 2 general gather kernel,
- * 3 pointer-array kernel, 4 scale-only kernel (alpha == 0 or k == 0);
+ * 3 pointer-array kernel, 4 scale-only kernel (alpha == 0 or k == 0),
+ * 5 register-direct kernel (packed square n <= 2);
  * +16 when a separate tail launch handled the last (< 16) pairs; +32 when the
  * kernel was a runtime-specialised (NVRTC, sm_100a) instance.  Also returns
  * the number of kernel launches of that call in *launches. */
@@ -223,6 +230,21 @@ int tx_set_jit(int enable);
 int tx_jit_compiled(void);
 /* Number of compiled kernel instances (AOT, size-specialised + generic). */
 int tx_num_instances(void);
+
+/* Layout classes for tx_prepare. */
+#define TX_LAYOUT_PACKED 0  /* strided, minimal leading dimensions (ld = rows, ld2 = rows*cols) */
+#define TX_LAYOUT_STRIDED 1 /* strided with padded ld / ld2 (the general gather kernel) */
+#define TX_LAYOUT_PTR 2     /* pointer arrays of packed matrices */
+/* Precompile: build (NVRTC) and load on the CURRENT device every runtime-
+ * specialised instance that a call of type `type` ('s','d','c','z'), ops
+ * transa/transb, sizes m, n, k, beta == 0 or not and layout class `layout`
+ * would use, so that the first real call does no compilation (a first-use
+ * compile otherwise takes seconds inside that call).  Launches nothing and
+ * dereferences no memory.  Returns 0 (also when NVRTC is unavailable: the AOT
+ * kernels need no preparation), -i for an invalid argument i (type -1,
+ * transa -2, transb -3, m -4, n -5, k -6, layout -8), or > 0 a CUDA error. */
+int tx_prepare(char type, char transa, char transb, int m, int n, int k, int beta_is_zero,
+               int layout);
 
 #ifdef __cplusplus
 }

@@ -54,11 +54,17 @@ def build(force: bool = False) -> str:
 
 
 def lib():
+    """The oracle library.  ORACLE_LIB=<path> loads another build of oracle.c instead
+    (used only by tests/test_oracle_mutations.py to run the pins against deliberately
+    broken variants)."""
     global _lib
     with _lock:
         if _lib is None:
-            build()
-            L = ctypes.CDLL(_LIB)
+            path = os.environ.get("ORACLE_LIB")
+            if not path:
+                build()
+                path = _LIB
+            L = ctypes.CDLL(path)
             vp, c_int, c_ll, c_char = ctypes.c_void_p, ctypes.c_int, ctypes.c_longlong, ctypes.c_char
             for k in KINDS:
                 f = getattr(L, f"oracle_gemm_batched_{k}")
@@ -69,10 +75,6 @@ def lib():
                 g.argtypes = [c_char, c_char, c_int, c_int, c_int, vp, vp, c_int, vp, c_int, vp, vp,
                               c_int, c_int]
                 g.restype = c_int
-                h = getattr(L, f"oracle_gemm_batched_x_{k}")
-                h.argtypes = [c_char, c_char, c_int, c_int, c_int, _SCALAR[k], _SCALAR[k], vp, c_int,
-                              c_ll, vp, c_int, c_ll, vp, vp, c_int, c_ll, c_int]
-                h.restype = None
             _lib = L
     return _lib
 
@@ -139,19 +141,3 @@ def gemm_batched_ptr(kind, transa, transb, m, n, k, alpha, A, a_offs, lda, B, b_
         pa, lda, pb, ldb, ctypes.addressof(b) if beta_ptr else None, pc, ldc, batch)
     del ka, kb, kc
     return rc
-
-
-def gemm_batched_x(kind, transa, transb, m, n, k, alpha, A, lda, lda2, B, ldb, ldb2, beta, C0,
-                   ldc, ldc2, batch):
-    """Long-double twin (self-check helper): returns a np.longdouble array of the
-    C layout's length (complex: 2 entries per element, re then im)."""
-    L = lib()
-    n_c = len(C0)
-    X = np.zeros(n_c * (2 if kind in ("c", "z") else 1), dtype=np.longdouble)
-    getattr(L, f"oracle_gemm_batched_x_{kind}")(
-        _op(transa), _op(transb), m, n, k, _scalar(kind, alpha), _scalar(kind, beta),
-        _ptr(A), lda, lda2, _ptr(B), ldb, ldb2, _ptr(C0), X.ctypes.data, ldc, ldc2, batch)
-    if kind in ("c", "z"):
-        return X[0::2] + 1j * X[1::2]
-    return X
-

@@ -34,10 +34,6 @@
  * (1-based) is invalid; the validation below is an independent re-implementation
  * of the rules listed in DESIGN.md §Boundary.
  *
- * A long-double twin (oracle_gemm_batched_x_*) evaluates the same loop in x87
- * extended precision and writes long double results; it is used only by the
- * oracle's own self-checks (error-bound pins).
- *
  * Parity status: every function here is pinned by tests/test_oracle_pins.py
  * (closed forms, hand cases, library routine, exact rational arithmetic,
  * invariants).  No function is "parity unpinned".
@@ -81,7 +77,7 @@ static int ranges_overlap(const void *p, long long np, const void *q, long long 
  *   transa -1, transb -2, m -3, n -4, k -5 (each in [0,32]), alpha NULL -6,
  *   beta NULL -13 [-11], lda -8, ldb -11 [-10], ldc -15 [-13],
  *   (batch > 1) lda2 < 0 -9, ldb2 < 0 -12, ldc2 < ldc*n -16  (Fig. 1),
- *   batch < 0 -17 [-14], A NULL -7, B NULL -10 [-9], C NULL -14 [-12],
+ *   batch < 0 -17 [-14], A NULL or misaligned -7, B -10 [-9], C -14 [-12],
  *   (strided) C's extent overlapping A's or B's -14.
  */
 static int validate(int ptr, char ta, char tb, int m, int n, int k,
@@ -110,9 +106,12 @@ static int validate(int ptr, char ta, char tb, int m, int n, int k,
     if (batch < 0) return ptr ? -14 : -17;
     int work = m > 0 && n > 0 && batch > 0;
     int reads_ab = work && !alpha_is_zero && k > 0;
-    if (reads_ab && A == NULL) return -7;
-    if (reads_ab && B == NULL) return ptr ? -9 : -10;
-    if (work && C == NULL) return ptr ? -12 : -14;
+    /* NULL, or an address that is not a multiple of the element size (pointer
+     * arrays: of the pointer size) -- DESIGN.md reading R21 */
+    size_t al = ptr ? sizeof(void *) : esz;
+    if (reads_ab && (A == NULL || (uintptr_t)A % al != 0)) return -7;
+    if (reads_ab && (B == NULL || (uintptr_t)B % al != 0)) return ptr ? -9 : -10;
+    if (work && (C == NULL || (uintptr_t)C % al != 0)) return ptr ? -12 : -14;
     if (!ptr && reads_ab) {
         long long ec = extent(m, n, ldc, ldc2, batch);
         if (ranges_overlap(C, ec, A, extent(rowsA, colsA, lda, lda2, batch), esz)) return -14;
@@ -282,77 +281,5 @@ int oracle_gemm_batched_ptr_##SUF(char ta, char tb, int m, int n, int k,        
 O_CPLX_API(c, o_cfloat)
 O_CPLX_API(z, o_cdouble)
 
-/* ------------------------------------------------- long-double twin (self-checks) */
-/*
- * Same definition, evaluated in long double.  Inputs in working precision;
- * C0 is the input C (read only when beta != 0); the result goes to X (long
- * double, same ldc/ldc2 layout; complex results as (re, im) pairs).  Packed
- * strided layout only; no validation (callers are the oracle's own tests).
- */
-#define O_REAL_X(SUF, T)                                                                 \
-void oracle_gemm_batched_x_##SUF(char ta, char tb, int m, int n, int k, T a, T b,        \
-                                 const T *A, int lda, long long lda2,                    \
-                                 const T *B, int ldb, long long ldb2,                    \
-                                 const T *C0, long double *X, int ldc, long long ldc2,   \
-                                 int batch)                                              \
-{                                                                                        \
-    for (int p = 0; p < batch; ++p)                                                      \
-        for (int j = 0; j < n; ++j)                                                      \
-            for (int i = 0; i < m; ++i) {                                                \
-                long double x = 0;                                                       \
-                for (int l = 0; l < k; ++l) {                                            \
-                    long double u = op_is_n(ta) ? A[lda2 * p + i + (long long)lda * l]   \
-                                                : A[lda2 * p + l + (long long)lda * i];  \
-                    long double v = op_is_n(tb) ? B[ldb2 * p + l + (long long)ldb * j]   \
-                                                : B[ldb2 * p + j + (long long)ldb * l];  \
-                    x += u * v;                                                          \
-                }                                                                        \
-                long long o = ldc2 * p + i + (long long)ldc * j;                         \
-                long double y = (long double)a * x;                                      \
-                if (b != 0) y += (long double)b * C0[o];                                 \
-                X[o] = y;                                                                \
-            }                                                                            \
-}
-
-O_REAL_X(s, float)
-O_REAL_X(d, double)
-
-#define O_CPLX_X(SUF, CT)                                                                \
-void oracle_gemm_batched_x_##SUF(char ta, char tb, int m, int n, int k, CT a, CT b,      \
-                                 const CT *A, int lda, long long lda2,                   \
-                                 const CT *B, int ldb, long long ldb2,                   \
-                                 const CT *C0, long double *X, int ldc, long long ldc2,  \
-                                 int batch)                                              \
-{                                                                                        \
-    for (int p = 0; p < batch; ++p)                                                      \
-        for (int j = 0; j < n; ++j)                                                      \
-            for (int i = 0; i < m; ++i) {                                                \
-                long double xr = 0, xi = 0;                                              \
-                for (int l = 0; l < k; ++l) {                                            \
-                    CT u = op_is_n(ta) ? A[lda2 * p + i + (long long)lda * l]            \
-                                       : A[lda2 * p + l + (long long)lda * i];           \
-                    CT v = op_is_n(tb) ? B[ldb2 * p + l + (long long)ldb * j]            \
-                                       : B[ldb2 * p + j + (long long)ldb * l];           \
-                    long double ur = u.re, ui = op_is_c(ta) ? -(long double)u.im : u.im; \
-                    long double vr = v.re, vi = op_is_c(tb) ? -(long double)v.im : v.im; \
-                    xr += ur * vr - ui * vi;                                             \
-                    xi += ur * vi + ui * vr;                                             \
-                }                                                                        \
-                long long o = ldc2 * p + i + (long long)ldc * j;                         \
-                long double yr = (long double)a.re * xr - (long double)a.im * xi;        \
-                long double yi = (long double)a.re * xi + (long double)a.im * xr;        \
-                if (!(b.re == 0 && b.im == 0)) {                                         \
-                    yr += (long double)b.re * C0[o].re - (long double)b.im * C0[o].im;   \
-                    yi += (long double)b.re * C0[o].im + (long double)b.im * C0[o].re;   \
-                }                                                                        \
-                X[2 * o] = yr;                                                           \
-                X[2 * o + 1] = yi;                                                       \
-            }                                                                            \
-}
-
-O_CPLX_X(c, o_cfloat)
-O_CPLX_X(z, o_cdouble)
-
 /* Sanity hooks for the Python wrapper. */
 int oracle_abi_version(void) { return 1; }
-int oracle_sizeof_long_double(void) { return (int)sizeof(long double); }

@@ -7,7 +7,7 @@ C-ABI library libtxgemm.so (include/txgemm.h, CUDA for sm_100a); this package
 is its thin binding (binding.py) plus the host-side work model (model.py).
 """
 from . import model  # noqa: F401
-from .binding import (TxError, build, gemm_batched, last_path, lib, num_instances, set_tuning,  # noqa: F401,E501
+from .binding import (TxError, build, gemm_batched, gemm_batched_ptr, last_path, prepare, lib, num_instances, set_tuning,  # noqa: F401,E501
                       pointer_array, set_max_ctas, status_string, tx_gemm_batched,
                       tx_gemm_batched_dev, tx_gemm_batched_hostio, tx_gemm_batched_ptr,
                       tx_gemm_batched_ptr_dev, version)
@@ -17,4 +17,4 @@ from .binding import (tx_gemm_batched_s, tx_gemm_batched_d, tx_gemm_batched_c,  
                       tx_gemm_batched_hostio_d, tx_gemm_batched_hostio_c,
                       tx_gemm_batched_hostio_z)
 
-__all__ = ["gemm_batched", "model", "lib", "build"]
+__all__ = ["gemm_batched", "gemm_batched_ptr", "prepare", "model", "lib", "build"]

@@ -23,7 +23,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("TXGEMM_LIB") or os.path.join(_HERE, "libtxgemm.so")
 
 KINDS = ("s", "d", "c", "z")
-PATHS = {0: "none", 1: "bulk", 2: "gather", 3: "ptr", 4: "scale", 17: "bulk+tail",
+PATHS = {0: "none", 1: "bulk", 2: "gather", 3: "ptr", 4: "scale", 5: "direct", 17: "bulk+tail",
          33: "bulk", 34: "gather", 35: "ptr", 49: "bulk+tail"}
 
 
@@ -97,6 +97,8 @@ def lib():
         L.tx_set_jit.argtypes = [ci]
         L.tx_set_jit.restype = ci
         L.tx_jit_compiled.restype = ci
+        L.tx_prepare.argtypes = [cc, cc, cc, ci, ci, ci, ci, ci]
+        L.tx_prepare.restype = ci
         _lib = L
         return L
 
@@ -178,6 +180,16 @@ def set_tuning(stages: int = 0, stage_kb: int = 0) -> int:
 
 def num_instances() -> int:
     return lib().tx_num_instances()
+
+
+LAYOUTS = {"packed": 0, "strided": 1, "ptr": 2}
+
+
+def prepare(kind, transa, transb, m, n, k, beta_zero=False, layout="packed") -> int:
+    """tx_prepare: build the runtime-specialised instances a call of this shape would
+    use on the current device, so the first real call does no compilation."""
+    return lib().tx_prepare(_op(kind), _op(transa), _op(transb), m, n, k, 1 if beta_zero else 0,
+                            LAYOUTS[layout] if isinstance(layout, str) else int(layout))
 
 
 # ------------------------------------------------------ raw C-ABI mirrors
@@ -269,9 +281,7 @@ def gemm_batched(A, B, C, transa="N", transb="N", alpha=1.0, beta=0.0, stream=No
     kind = kind_of(C.dtype)
     if A.dtype != C.dtype or B.dtype != C.dtype:
         raise ValueError("A, B and C must share a dtype")
-    for X in (A, B, C):
-        if not X.is_cuda:
-            raise ValueError("A, B, C must be CUDA tensors (no CPU fallback)")
+    _same_device(A=A, B=B, C=C)
     batch, m, n = C.shape
     k = A.shape[2] if transa in "nN" else A.shape[1]
     ra, ca = (m, k) if transa in "nN" else (k, m)
@@ -288,6 +298,54 @@ def gemm_batched(A, B, C, transa="N", transb="N", alpha=1.0, beta=0.0, stream=No
     with torch.cuda.device(C.device):
         return _check(tx_gemm_batched(kind, transa, transb, m, n, k, alpha, A, lda, lda2, B, ldb,
                                       ldb2, beta, C, ldc, ldc2, batch, stream))
+
+
+def _same_device(**tensors):
+    """All tensors are CUDA tensors on one device (the library works on the current
+    device; a tensor elsewhere would be a wild address there)."""
+    dev = None
+    for name, X in tensors.items():
+        if not X.is_cuda:
+            raise ValueError(f"{name} must be a CUDA tensor (no CPU fallback)")
+        if dev is None:
+            dev = X.device
+        elif X.device != dev:
+            raise ValueError(f"{name} is on {X.device}, expected {dev}")
+    return dev
+
+
+def gemm_batched_ptr(Aarray, Barray, Carray, m, n, k, transa="N", transb="N", alpha=1.0,
+                     beta=0.0, lda=None, ldb=None, ldc=None, dtype=None, stream=None):
+    """Pointer-array batch (the paper's TGEMM_multi_nounif):
+    C^p <- alpha*op(A^p) op(B^p) + beta*C^p with X^p at the device address Xarray[p].
+
+    Xarray are int64 CUDA tensors of device addresses (e.g. from pointer_array()),
+    all on one device; ``dtype`` is the matrices' torch dtype; ld* default to the
+    stored rows (packed matrices).  The pointed-to matrices must live on that device
+    and be aligned to the element size; C^p must not overlap each other or A, B
+    (include/txgemm.h)."""
+    import torch
+
+    if dtype is None:
+        raise ValueError("dtype of the matrices is required")
+    kind = kind_of(dtype)
+    dev = _same_device(Aarray=Aarray, Barray=Barray, Carray=Carray)
+    for name, X in (("Aarray", Aarray), ("Barray", Barray), ("Carray", Carray)):
+        if X.dtype != torch.int64 or X.dim() != 1:
+            raise ValueError(f"{name} must be a 1-D int64 tensor of device addresses")
+        if not X.is_contiguous():
+            raise ValueError(f"{name} must be contiguous")
+    batch = Carray.shape[0]
+    if Aarray.shape[0] < batch or Barray.shape[0] < batch:
+        raise ValueError("pointer arrays shorter than Carray")
+    ra = m if transa in "nN" else k
+    rb = k if transb in "nN" else n
+    lda = max(1, ra) if lda is None else lda
+    ldb = max(1, rb) if ldb is None else ldb
+    ldc = max(1, m) if ldc is None else ldc
+    with torch.cuda.device(dev):
+        return _check(tx_gemm_batched_ptr(kind, transa, transb, m, n, k, alpha, Aarray, lda,
+                                          Barray, ldb, beta, Carray, ldc, batch, stream))
 
 
 def pointer_array(X, offsets=None):

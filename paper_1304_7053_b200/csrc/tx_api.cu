@@ -86,6 +86,8 @@ int num_sms()
 
 static thread_local int t_last_path = 0;
 static thread_local int t_last_launches = 0;
+static thread_local bool t_prepare = false;
+bool prepare_only() { return t_prepare; }
 
 // ---------------------------------------------------------------- scalars
 template <class U> struct Api;
@@ -176,9 +178,14 @@ static int validate(bool ptr, char ta, char tb, int m, int n, int k, const void 
     if (batch < 0) return ptr ? -14 : -17;
     const bool work = m > 0 && n > 0 && batch > 0;
     const bool reads_ab = work && !alpha_zero && k > 0;
-    if (reads_ab && !A) return -7;
-    if (reads_ab && !B) return ptr ? -9 : -10;
-    if (work && !C) return ptr ? -12 : -14;
+    // NULL, or not aligned to the element size (s 4, d 8, c 8, z 16 bytes: the
+    // kernels move whole elements / element pairs); the pointer arrays themselves
+    // must be aligned to 8 bytes
+    const size_t al = ptr ? sizeof(void *) : es;
+    auto bad = [al](const void *q) { return !q || ((uintptr_t)q % al) != 0; };
+    if (reads_ab && bad(A)) return -7;
+    if (reads_ab && bad(B)) return ptr ? -9 : -10;
+    if (work && bad(C)) return ptr ? -12 : -14;
     if (!ptr && reads_ab) {
         const long long ec = extent_elems(m, n, ldc, ldc2, batch);
         if (overlap(C, ec, A, extent_elems(rowsA, colsA, lda, lda2, batch), es)) return -14;
@@ -237,6 +244,20 @@ bool encode_tma_rows(TmaDesc *d, const void *base, int es, int k, long long rows
 }
 
 static int as_status(cudaError_t e) { return e == cudaSuccess ? 0 : (int)e; }
+
+// Register-direct kernel for n <= 2 (TX_DIRECT=0 disables it: A/B measurements).
+static bool direct_enabled()
+{
+    static const bool on = [] {
+        const char *v = getenv("TX_DIRECT");
+        return !(v && v[0] == '0');
+    }();
+    return on;
+}
+
+// Pairs per bulk launch (a multiple of every 16-byte alignment unit): keeps the
+// 32-bit TMA row coordinates pair * rows (rows <= 32) below 2^31.
+constexpr long long BULK_CHUNK_PAIRS = 1ll << 26;
 
 // ------------------------------------------------------------- strided call
 template <class U>
@@ -331,16 +352,29 @@ static int gemm_strided(char ta, char tb, int m, int n, int k, const U *alpha, c
             }
         }
     }
+    if (packed && m == n && n == k && m <= 2 && direct_enabled()) {
+        // tiny matrices: register-direct kernel, whole batch (tail included)
+        const cudaError_t e = tab.direct[opa][opb][b0][m - 1](&p, st);
+        if (e != cudaSuccess) return as_status(e);
+        t_last_path = PATH_DIRECT;
+        t_last_launches = 1;
+        return 0;
+    }
     if (packed) {
         const int es = (int)sizeof(U);
         const int unit = 16 / gcd_i(16, gcd_i((int)(SA * es), gcd_i((int)(SB * es), (int)(SC * es))));
         const int main_pairs = batch / unit * unit;
-        if (main_pairs > 0) {
+        // Launches of at most BULK_CHUNK_PAIRS pairs: the TMA tensor-copy
+        // coordinates (row = pair * rows, 32-bit) stay below 2^31 for rows <= 32.
+        for (long long c0 = 0; c0 < main_pairs; c0 += BULK_CHUNK_PAIRS) {
             Params<T> q = p;
-            q.batch = main_pairs;
+            q.batch = (int)std::min<long long>(BULK_CHUNK_PAIRS, main_pairs - c0);
             q.lda2 = SA;
             q.ldb2 = SB;
             q.ldc2 = SC;
+            q.A += SA * c0;
+            q.B += SB * c0;
+            q.C += SC * c0;
             LaunchFn fn = (m == n && n == k && m <= 16) ? tab.bulk_sq[opa][opb][b0][m - 1] : nullptr;
             cudaError_t e = cudaErrorNotSupported;
             path = PATH_BULK;
@@ -348,7 +382,10 @@ static int gemm_strided(char ta, char tb, int m, int n, int k, const U *alpha, c
                 e = launch_jit<T>(JIT_BULK, q, opa, opb, b0, st);
                 if (e == cudaSuccess) path |= PATH_JIT;
             }
-            if (e == cudaErrorNotSupported) e = (fn ? fn : tab.bulk_dyn[opa][opb][b0])(&q, st);
+            if (e == cudaErrorNotSupported && fn) e = fn(&q, st);
+            // (an AOT tensor-copy instance whose tensor map cannot be encoded also
+            // reports cudaErrorNotSupported: the generic bulk kernel takes over)
+            if (e == cudaErrorNotSupported) e = tab.bulk_dyn[opa][opb][b0](&q, st);
             if (e != cudaSuccess) return as_status(e);
             ++launches;
         }
@@ -620,9 +657,10 @@ static int gemm_hostio(char ta, char tb, int m, int n, int k, const U *alpha, co
     const U a = *alpha, b = *beta;
     const bool work = m > 0 && n > 0 && batch > 0;
     const bool reads_ab = work && !AT::zero(a) && k > 0;
-    if (reads_ab && !dA) return -19;
-    if (reads_ab && !dB) return -20;
-    if (work && !dC) return -21;
+    auto bad = [](const void *q) { return !q || ((uintptr_t)q % sizeof(U)) != 0; };
+    if (reads_ab && bad(dA)) return -19;
+    if (reads_ab && bad(dB)) return -20;
+    if (work && bad(dC)) return -21;
     if (!work || ((AT::zero(a) || k == 0) && AT::one(b))) {
         t_last_path = PATH_NONE;
         t_last_launches = 0;
@@ -702,9 +740,72 @@ static int gemm_hostio(char ta, char tb, int m, int n, int k, const U *alpha, co
     return 0;
 }
 
+// ------------------------------------------------------------ tx_prepare
+// Runs the dispatch of a call of this shape on placeholder (never dereferenced)
+// addresses with launches suppressed: every runtime-specialised instance the
+// call would use is compiled and loaded on the current device, and every AOT
+// kernel's attributes are set, so a later call of this shape does no NVRTC work.
+template <class U>
+static int prepare(char ta, char tb, int m, int n, int k, bool b0, int layout)
+{
+    using AT = Api<U>;
+    U one, half, zero;
+    std::memset(&one, 0, sizeof(U));
+    std::memset(&zero, 0, sizeof(U));
+    std::memset(&half, 0, sizeof(U));
+    *reinterpret_cast<typename std::conditional<AT::cplx, typename std::conditional<
+        sizeof(U) == 8, float, double>::type, U>::type *>(&one) = 1;
+    *reinterpret_cast<typename std::conditional<AT::cplx, typename std::conditional<
+        sizeof(U) == 8, float, double>::type, U>::type *>(&half) = 0.5;
+    const U *beta = b0 ? &zero : &half;
+    const int batch = 1 << 20;
+    const int rowsA = op_n(ta) ? m : k, colsA = op_n(ta) ? k : m;
+    const int rowsB = op_n(tb) ? k : n, colsB = op_n(tb) ? n : k;
+    const int pad = layout == TX_LAYOUT_STRIDED ? 1 : 0;
+    const int lda = max1(rowsA) + pad, ldb = max1(rowsB) + pad, ldc = max1(m) + pad;
+    const long long lda2 = (long long)lda * colsA + pad, ldb2 = (long long)ldb * colsB + pad,
+                    ldc2 = (long long)ldc * n + pad;
+    // disjoint, 4 KB-aligned placeholder ranges (1 TB apart)
+    U *A = reinterpret_cast<U *>(uintptr_t(1) << 40), *B = reinterpret_cast<U *>(uintptr_t(2) << 40),
+      *C = reinterpret_cast<U *>(uintptr_t(3) << 40);
+    t_prepare = true;
+    int rc;
+    if (layout == TX_LAYOUT_PTR)
+        rc = gemm_ptr<U>(ta, tb, m, n, k, &one, reinterpret_cast<const U *const *>(A), lda,
+                         reinterpret_cast<const U *const *>(B), ldb, beta,
+                         reinterpret_cast<U *const *>(C), ldc, batch, 0);
+    else
+        rc = gemm_strided<U>(ta, tb, m, n, k, &one, A, lda, lda2, B, ldb, ldb2, beta, C, ldc,
+                             ldc2, batch, 0);
+    t_prepare = false;
+    t_last_path = PATH_NONE;
+    t_last_launches = 0;
+    // validation codes of the inner call map to tx_prepare's own positions
+    if (rc == -1) return -2;
+    if (rc == -2) return -3;
+    if (rc == -3) return -4;
+    if (rc == -4) return -5;
+    if (rc == -5) return -6;
+    return rc < 0 ? -8 : rc;
+}
+
 }  // namespace tx
 
 // ====================================================================== C ABI
+extern "C" int tx_prepare(char type, char transa, char transb, int m, int n, int k,
+                          int beta_is_zero, int layout)
+{
+    if (layout != TX_LAYOUT_PACKED && layout != TX_LAYOUT_STRIDED && layout != TX_LAYOUT_PTR)
+        return -8;
+    switch (type) {
+    case 's': case 'S': return tx::prepare<float>(transa, transb, m, n, k, beta_is_zero != 0, layout);
+    case 'd': case 'D': return tx::prepare<double>(transa, transb, m, n, k, beta_is_zero != 0, layout);
+    case 'c': case 'C': return tx::prepare<tx_cfloat>(transa, transb, m, n, k, beta_is_zero != 0, layout);
+    case 'z': case 'Z': return tx::prepare<tx_cdouble>(transa, transb, m, n, k, beta_is_zero != 0, layout);
+    default: return -1;
+    }
+}
+
 using namespace tx;
 
 #define TX_STRIDED(SUF, U)                                                                        \

@@ -17,7 +17,11 @@ void fill_ops(TypeTables &t)
     t.bulk_dyn_dev[OPA][OPB] = &launch_bulk_dev<TxT, OPA, OPB>;
     t.gather_dev[OPA][OPB][0] = &launch_gather_dev<TxT, OPA, OPB, false>;
     t.gather_dev[OPA][OPB][1] = &launch_gather_dev<TxT, OPA, OPB, true>;
-    t.count += 9;
+    t.direct[OPA][OPB][0][0] = &launch_direct<TxT, 1, OPA, OPB, false>;
+    t.direct[OPA][OPB][1][0] = &launch_direct<TxT, 1, OPA, OPB, true>;
+    t.direct[OPA][OPB][0][1] = &launch_direct<TxT, 2, OPA, OPB, false>;
+    t.direct[OPA][OPB][1][1] = &launch_direct<TxT, 2, OPA, OPB, true>;
+    t.count += 13;
 }
 }  // namespace
 

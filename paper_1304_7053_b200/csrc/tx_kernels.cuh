@@ -569,8 +569,8 @@ __global__ void __launch_bounds__(NT) bulk_kernel(const __grid_constant__ Params
 // ring, issued by the 32 lanes of warp 0 (lane q copies matrices q, q+32, ...),
 // with the tile's pointers prefetched one iteration ahead so the pointer loads
 // never stall the issue.  A matrix whose pointer is not 16-byte aligned is
-// copied synchronously by its lane instead (ordered before its use by the
-// end-of-iteration barrier; its bytes are excluded from the expected count).
+// copied synchronously by its lane instead, before lane 0 arrives on the stage's
+// mbarrier (its bytes are excluded from the expected count).
 // P <= 32 * PPL pairs per tile.
 // --------------------------------------------------------------------------
 template <class T, int MS, int NS, int KS, int OPA, int OPB, bool B0, class MP, int NT>
@@ -625,22 +625,37 @@ __global__ void __launch_bounds__(NT) bulk_ptr_kernel(const Params<T> p)
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
-        if (lane == 0) mbar_arrive_expect_tx(bar, mine);
-        __syncwarp();
+        // (1) matrices whose pointer is not 16-byte aligned: synchronous copies,
+        // completed by every lane BEFORE lane 0's arrive (release) so that a thread
+        // passing mbar_wait (acquire) sees them -- even when the whole tile is
+        // unaligned and the expected byte count is 0.  The async-proxy fence
+        // orders these generic writes before later bulk copies into the stage.
+        bool sync_copied = false;
 #pragma unroll
         for (int r = 0; r < PPL; ++r) {
             const int q = lane + 32 * r;
-            auto copy = [&](T *dst, const T *src, uint32_t bytes, int elems) {
-                if (!src) return;
-                if (((uintptr_t)src & 15) == 0) {
-                    bulk_g2s(dst, src, bytes, bar, pol);
-                } else {
-                    for (int e = 0; e < elems; ++e) dst[e] = src[e];
-                }
+            auto copy_sync = [&](T *dst, const T *src, int elems) {
+                if (!src || ((uintptr_t)src & 15) == 0) return;
+                for (int e = 0; e < elems; ++e) dst[e] = src[e];
+                sync_copied = true;
             };
-            copy(st + q * SA, pa[r], ba, SA);
-            copy(st + P * SA + q * SB, pb[r], bb, SB);
-            if (!B0) copy(st + P * (SA + SB) + q * SC, pc[r], bc, SC);
+            copy_sync(st + q * SA, pa[r], SA);
+            copy_sync(st + P * SA + q * SB, pb[r], SB);
+            if (!B0) copy_sync(st + P * (SA + SB) + q * SC, pc[r], SC);
+        }
+        if (sync_copied) fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_expect_tx(bar, mine);
+        // (2) the aligned matrices: one bulk async copy each, counted on the barrier
+#pragma unroll
+        for (int r = 0; r < PPL; ++r) {
+            const int q = lane + 32 * r;
+            auto copy_async = [&](T *dst, const T *src, uint32_t bytes) {
+                if (src && ((uintptr_t)src & 15) == 0) bulk_g2s(dst, src, bytes, bar, pol);
+            };
+            copy_async(st + q * SA, pa[r], ba);
+            copy_async(st + P * SA + q * SB, pb[r], bb);
+            if (!B0) copy_async(st + P * (SA + SB) + q * SC, pc[r], bc);
         }
     };
 
@@ -881,6 +896,117 @@ __global__ void __launch_bounds__(NT) gather_kernel(const Params<T> p)
         }
     }
     cp_async_wait<0>();
+}
+
+// --------------------------------------------------------------------------
+// Tiny square matrices (n <= 2), packed and 16-byte aligned: register-direct.
+// A pair's matrices are 4..64 bytes, so staging them through shared memory buys
+// nothing (no reuse across threads) and the kernel is all latency: every thread
+// owns G consecutive pairs (G*n*n*sizeof(T) a multiple of 16 bytes), loads its
+// A, B (C) bytes with 16-byte streaming loads straight into registers -- all of
+// a unit's loads in flight at once, the next unit's issued before this one is
+// computed -- computes the n x n products with the same ascending-l FMA chain
+// and epilogue as micro_tile (so results are bitwise identical to the other
+// kernels), and stores C with 16-byte streaming stores.  The last batch % G
+// pairs are done element by element by the first threads.
+// --------------------------------------------------------------------------
+template <class T, int N>
+struct DirectShape {
+    static constexpr int E = N * N;                                      // elements per matrix
+    static constexpr int ES = (int)sizeof(T);
+    static constexpr int G = E * ES >= 16 ? 1 : 16 / (E * ES);           // pairs per unit
+    static constexpr int CH = G * E * ES / 16;                           // 16-byte chunks per operand
+    static_assert((G * E * ES) % 16 == 0, "direct unit must be whole 16-byte chunks");
+};
+
+__device__ __forceinline__ uint4 ld_stream16(const void *p)
+{
+    uint4 r;
+    asm volatile("ld.global.cs.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+    return r;
+}
+__device__ __forceinline__ void st_stream16(void *p, uint4 v)
+{
+    asm volatile("st.global.cs.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y),
+                 "r"(v.z), "r"(v.w)
+                 : "memory");
+}
+
+// One pair: c[i + N*j] <- alpha * sum_l op(a)_il op(b)_lj (+ beta * c[i + N*j]).
+template <class T, int N, int OPA, int OPB, bool B0>
+__device__ __forceinline__ void direct_pair(const T *a, const T *b, T *c, T alpha, T beta)
+{
+    constexpr bool CA = OPA == OP_C, CB = OPB == OP_C;
+#pragma unroll
+    for (int j = 0; j < N; ++j)
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+            T acc = zero<T>();
+#pragma unroll
+            for (int l = 0; l < N; ++l)
+                mac<CA, CB>(acc, OPA == OP_N ? a[i + N * l] : a[l + N * i],
+                            OPB == OP_N ? b[l + N * j] : b[j + N * l]);
+            c[i + N * j] = B0 ? ax(alpha, acc) : axpby(alpha, acc, beta, c[i + N * j]);
+        }
+}
+
+template <class T, int N, int OPA, int OPB, bool B0, int NT>
+__global__ void __launch_bounds__(NT) direct_kernel(const __grid_constant__ Params<T> p)
+{
+    using SH = DirectShape<T, N>;
+    constexpr int E = SH::E, G = SH::G, CH = SH::CH;
+    grid_dep_wait();
+    grid_dep_launch();
+    const T alpha = p.alpha, beta = p.beta;
+    const long long units = p.batch / G;
+    const long long stride = (long long)gridDim.x * NT;
+    const uint4 *gA = reinterpret_cast<const uint4 *>(p.A);
+    const uint4 *gB = reinterpret_cast<const uint4 *>(p.B);
+    uint4 *gC = reinterpret_cast<uint4 *>(p.C);
+    for (long long u = (long long)blockIdx.x * NT + threadIdx.x; u < units; u += 2 * stride) {
+        // two units per trip, all loads issued before any arithmetic
+        const long long u2 = u + stride;
+        const bool two = u2 < units;
+        T a[2][G * E], b[2][G * E], c[2][G * E];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const long long uu = h ? (two ? u2 : u) : u;
+#pragma unroll
+            for (int q = 0; q < CH; ++q) {
+                reinterpret_cast<uint4 *>(a[h])[q] = ld_stream16(gA + uu * CH + q);
+                reinterpret_cast<uint4 *>(b[h])[q] = ld_stream16(gB + uu * CH + q);
+                if constexpr (!B0) reinterpret_cast<uint4 *>(c[h])[q] = ld_stream16(gC + uu * CH + q);
+            }
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            if (h == 1 && !two) break;
+#pragma unroll
+            for (int g = 0; g < G; ++g)
+                direct_pair<T, N, OPA, OPB, B0>(a[h] + g * E, b[h] + g * E, c[h] + g * E, alpha,
+                                                 beta);
+            const long long uu = h ? u2 : u;
+#pragma unroll
+            for (int q = 0; q < CH; ++q) st_stream16(gC + uu * CH + q, reinterpret_cast<uint4 *>(c[h])[q]);
+        }
+    }
+    // the last batch % G pairs, one per thread of the first block
+    const long long tail0 = units * G;
+    if (blockIdx.x == 0 && tail0 + threadIdx.x < p.batch) {
+        const long long q = tail0 + threadIdx.x;
+        T a[E], b[E], c[E];
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            a[e] = p.A[q * E + e];
+            b[e] = p.B[q * E + e];
+            if constexpr (!B0) c[e] = p.C[q * E + e];
+        }
+        direct_pair<T, N, OPA, OPB, B0>(a, b, c, alpha, beta);
+#pragma unroll
+        for (int e = 0; e < E; ++e) p.C[q * E + e] = c[e];
+    }
 }
 
 // --------------------------------------------------------------------------

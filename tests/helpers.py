@@ -106,3 +106,23 @@ def random_case(kind, m, n, k, batch, transa="N", transb="N", seed=1, tag="case"
     B = Operand(kind, rb, cb, batch, key("B"), pad[0], pad[1], dist)
     C = Operand(kind, m, n, batch, key("C"), pad[0], pad[1], dist, sentinel=c_sentinel)
     return A, B, C
+
+
+def dense_at(buf, offs, rows, cols, ld):
+    """(batch, rows, cols) copy of the matrices starting at element offsets offs
+    (pointer-array layouts), column-major with leading dimension ld."""
+    offs = np.asarray(offs, dtype=np.int64)[:, None, None]
+    i = np.arange(rows)[None, :, None]
+    j = np.arange(cols)[None, None, :]
+    return buf[offs + i + ld * j]
+
+
+def denominators_dense(kind, transa, transb, alpha, beta, Ad, Bd, C0d):
+    """Element-wise |alpha| sum_l |op(A)_il||op(B)_lj| + |beta||C0_ij| from dense stored
+    (batch, rows, cols) arrays."""
+    a = np.abs(op_dense(np.asarray(Ad).astype(WIDE[kind]), transa))
+    b = np.abs(op_dense(np.asarray(Bd).astype(WIDE[kind]), transb))
+    d = abs(alpha) * np.einsum("pil,plj->pij", a, b)
+    if beta != 0:
+        d = d + abs(beta) * np.abs(np.asarray(C0d).astype(WIDE[kind]))
+    return d

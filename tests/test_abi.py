@@ -62,6 +62,7 @@ BAD = [
     dict(ldb=2), dict(ldc=1), dict(lda2=-5), dict(ldb2=-1), dict(ldc2=15), dict(batch=-2),
     dict(A=None), dict(B=None), dict(C=None), dict(C=FAKE + 8),  # C overlaps A
     dict(C=FAKE + (1 << 20) + 40),  # C overlaps B
+    dict(A=FAKE + 2), dict(B=FAKE + (1 << 20) + 2), dict(C=FAKE + (2 << 20) + 2),  # misaligned
 ]
 
 
@@ -128,3 +129,38 @@ def test_hostio_staging_checks():
              None, FAKE) == -20
     assert f("s", "N", "N", 2, 2, 2, 1, hp, 2, 4, hp + 64, 2, 4, 0, hp + 128, 2, 4, 2, 0, FAKE,
              FAKE, None) == -21
+
+
+def test_z_needs_16_byte_alignment():
+    """tx_cdouble matrices 8-byte aligned (legal for the C struct) are rejected: the
+    kernels move 16-byte elements (R21)."""
+    f = tx.tx_gemm_batched
+    assert f("z", "N", "N", 4, 4, 4, 1, FAKE + 8, 4, 16, FAKE + (1 << 20), 4, 16, 0,
+             FAKE + (2 << 20), 4, 16, 3, stream=0) == -7
+    assert f("z", "N", "N", 4, 4, 4, 1, FAKE, 4, 16, FAKE + (1 << 20) + 8, 4, 16, 0,
+             FAKE + (2 << 20), 4, 16, 3, stream=0) == -10
+    assert f("z", "N", "N", 4, 4, 4, 1, FAKE, 4, 16, FAKE + (1 << 20), 4, 16, 0,
+             FAKE + (2 << 20) + 8, 4, 16, 3, stream=0) == -14
+    # pointer arrays must be 8-byte aligned
+    g = tx.tx_gemm_batched_ptr
+    assert g("d", "N", "N", 2, 2, 2, 1, FAKE + 4, 2, FAKE, 2, 0, FAKE, 2, 1, 0) == -7
+    assert g("d", "N", "N", 2, 2, 2, 1, FAKE, 2, FAKE + 4, 2, 0, FAKE, 2, 1, 0) == -9
+    assert g("d", "N", "N", 2, 2, 2, 1, FAKE, 2, FAKE, 2, 0, FAKE + 4, 2, 1, 0) == -12
+    # host-buffer staging buffers likewise
+    h = tx.tx_gemm_batched_hostio
+    hb = np.zeros(4096, dtype=np.complex128)
+    hp = (hb.ctypes.data + 63) // 64 * 64
+    assert h("z", "N", "N", 2, 2, 2, 1, hp, 2, 4, hp + 1024, 2, 4, 0, hp + 2048, 2, 4, 2, 0,
+             FAKE + 8, FAKE, FAKE) == -19
+
+
+def test_prepare_argument_errors():
+    """tx_prepare validates before touching the device (no GPU needed)."""
+    assert tx.prepare("q", "N", "N", 4, 4, 4) == -1
+    assert tx.prepare("s", "x", "N", 4, 4, 4) == -2
+    assert tx.prepare("d", "N", "?", 4, 4, 4) == -3
+    assert tx.prepare("c", "N", "N", 33, 4, 4) == -4
+    assert tx.prepare("z", "N", "N", 4, -1, 4) == -5
+    assert tx.prepare("s", "N", "N", 4, 4, 99) == -6
+    assert tx.prepare("s", "N", "N", 4, 4, 4, layout=7) == -8
+    assert tx.prepare("s", "N", "N", 0, 4, 4) == 0  # quick return: nothing to build

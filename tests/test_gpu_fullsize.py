@@ -111,6 +111,23 @@ def test_config1_small():
     assert err <= TOL[kind]
 
 
+OPS = {"s": "NT", "d": "NT", "c": "NTC", "z": "NTC"}
+
+
+@pytest.mark.parametrize("kind", "sdcz")
+@pytest.mark.parametrize("n", range(1, 17))
+def test_config3_all_ops_1e5_sampled(kind, n):
+    """BASELINE configs[2] at its real size: 100,000 pairs for every type, n = 1..16,
+    every op pair and both epilogues, in the
+    launch configuration the sweep times (automatic grid, many tiles per CTA)."""
+    for ta in OPS[kind]:
+        for tb in OPS[kind]:
+            for general in (False, True):
+                err, path = run_full(kind, n, n, n, 100_000, ta, tb, general, samples=256,
+                                     seed=n)
+                assert path[0] == ("direct" if n <= 2 else "bulk"), path
+
+
 @pytest.mark.parametrize("kind", "sdcz")
 def test_gate_size_1e6_sampled(kind):
     """North-star gate workload: 10^6 pairs of 16x16, beta == 0 and general."""

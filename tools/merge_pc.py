@@ -21,7 +21,7 @@ def load(f):
 def main():
     c1, p1, c2, p2 = (load(f) for f in sys.argv[1:5])
     pat = re.compile(r"TX_MAP\((\w+), (\d+), (\d), (\d), (\d), ")
-    pc_lines = {pat.match(l).groups(): l for l in open("paper_1304_7053_b200/csrc/tx_map_table_pc.inc")
+    pc_lines = {pat.match(l).groups(): l for l in open("tools/archive/tables/tx_map_table_pc.inc")
                 if pat.match(l)}
     tra = set()  # (T, n, opb, b0) whose op(A) = N mapping a TRA instance borrows
     asw = {m.groups()[:5] for m in (re.match(r"TX_ASWMAP\((\w+), (\d+), (\d), (\d), (\d), .*, 1\)", l)
