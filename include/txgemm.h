@@ -7,7 +7,9 @@
  *
  *   op(X) = X, X^T or X^* selected by 'N'/'n', 'T'/'t', 'C'/'c' (PAPER.md:240-243,
  *   344-345); for the real types 'C' is the same as 'T'.  C^p is m x n, op(A^p) is
- *   m x k, op(B^p) is k x n; 0 <= m, n, k <= 32.  Sizes up to
+ *   m x k, op(B^p) is k x n; 0 <= m, n, k <= 64 for s and d,
+ *   <= 32 for c and z (TX_MAX_DIM, TX_MAX_DIM_CPLX: about the FP32 / FP64 ridge
+ *   point of each type, where the path stops being HBM-bound).  Sizes up to
  *   16 are the paper's regime and have ahead-of-time size-
  *   specialised kernels for square shapes; larger ones are the paper's "easily
  *   extended to larger sizes", served by runtime-
@@ -53,7 +55,8 @@
  * call) is invalid -- nothing is enqueued and C is untouched; > 0 a cudaError_t
  * raised while launching.  Argument checks, in order (strided positions, the
  * pointer call's positions in brackets):
- *   transa -1, transb -2, m -3, n -4, k -5 (outside [0,32]), alpha NULL -6,
+ *   transa -1, transb -2, m -3, n -4, k -5 (outside [0, TX_MAX_DIM] for s/d,
+ *   [0, TX_MAX_DIM_CPLX] for c/z), alpha NULL -6,
  *   beta NULL -13 [-11], lda < max(1, rows of stored A) -8,
  *   ldb < max(1, rows of stored B) -11 [-10], ldc < max(1, m) -15 [-13];
  *   batch_count > 1 (strided only): lda2 < 0 -9, ldb2 < 0 -12, ldc2 < ldc*n -16;
@@ -81,7 +84,8 @@ typedef struct { double re, im; } tx_cdouble;
 typedef struct CUstream_st *tx_stream_t;
 
 #define TX_VERSION 10100 /* 1.1.0 */
-#define TX_MAX_DIM 32
+#define TX_MAX_DIM 64       /* s, d */
+#define TX_MAX_DIM_CPLX 32  /* c, z */
 
 /* ---- strided batch: TGEMM_multi_uniform. Args 1..18. ---- */
 int tx_gemm_batched_s(char transa, char transb, int m, int n, int k,

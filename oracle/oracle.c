@@ -44,7 +44,8 @@
 typedef struct { float re, im; } o_cfloat;
 typedef struct { double re, im; } o_cdouble;
 
-#define O_MAXDIM 32
+#define O_MAXDIM_REAL 64 /* s, d (reading R14) */
+#define O_MAXDIM_CPLX 32 /* c, z */
 
 /* ---------------------------------------------------------------- helpers */
 
@@ -74,7 +75,8 @@ static int ranges_overlap(const void *p, long long np, const void *q, long long 
 /*
  * Argument checks, in the order of DESIGN.md §Boundary (argument positions of
  * the strided call; the pointer call's positions in brackets):
- *   transa -1, transb -2, m -3, n -4, k -5 (each in [0,32]), alpha NULL -6,
+ *   transa -1, transb -2, m -3, n -4, k -5 (each in [0,64] for s/d, [0,32] for c/z),
+ *   alpha NULL -6,
  *   beta NULL -13 [-11], lda -8, ldb -11 [-10], ldc -15 [-13],
  *   (batch > 1) lda2 < 0 -9, ldb2 < 0 -12, ldc2 < ldc*n -16  (Fig. 1),
  *   batch < 0 -17 [-14], A NULL or misaligned -7, B -10 [-9], C -14 [-12],
@@ -84,13 +86,14 @@ static int validate(int ptr, char ta, char tb, int m, int n, int k,
                     const void *alpha, int alpha_is_zero, const void *beta,
                     const void *A, int lda, long long lda2,
                     const void *B, int ldb, long long ldb2,
-                    const void *C, int ldc, long long ldc2, int batch, size_t esz)
+                    const void *C, int ldc, long long ldc2, int batch, size_t esz,
+                    int maxdim)
 {
     if (!op_valid(ta)) return -1;
     if (!op_valid(tb)) return -2;
-    if (m < 0 || m > O_MAXDIM) return -3;
-    if (n < 0 || n > O_MAXDIM) return -4;
-    if (k < 0 || k > O_MAXDIM) return -5;
+    if (m < 0 || m > maxdim) return -3;
+    if (n < 0 || n > maxdim) return -4;
+    if (k < 0 || k > maxdim) return -5;
     if (alpha == NULL) return -6;
     if (beta == NULL) return ptr ? -11 : -13;
     int rowsA = op_is_n(ta) ? m : k, colsA = op_is_n(ta) ? k : m;
@@ -159,7 +162,7 @@ int oracle_gemm_batched_##SUF(char ta, char tb, int m, int n, int k, const T *al
                               T *C, int ldc, long long ldc2, int batch)                 \
 {                                                                                       \
     int rc = validate(0, ta, tb, m, n, k, alpha, alpha && *alpha == 0, beta, A, lda,    \
-                      lda2, B, ldb, ldb2, C, ldc, ldc2, batch, sizeof(T));              \
+                      lda2, B, ldb, ldb2, C, ldc, ldc2, batch, sizeof(T), O_MAXDIM_REAL);              \
     if (rc) return rc;                                                                  \
     T a = *alpha, b = *beta;                                                            \
     if (m == 0 || n == 0 || batch == 0 || ((a == 0 || k == 0) && b == 1)) return 0;     \
@@ -175,7 +178,7 @@ int oracle_gemm_batched_ptr_##SUF(char ta, char tb, int m, int n, int k, const T
                                   T *const *Carray, int ldc, int batch)                 \
 {                                                                                       \
     int rc = validate(1, ta, tb, m, n, k, alpha, alpha && *alpha == 0, beta, Aarray,    \
-                      lda, 0, Barray, ldb, 0, Carray, ldc, 0, batch, sizeof(T));        \
+                      lda, 0, Barray, ldb, 0, Carray, ldc, 0, batch, sizeof(T), O_MAXDIM_REAL);        \
     if (rc) return rc;                                                                  \
     T a = *alpha, b = *beta;                                                            \
     if (m == 0 || n == 0 || batch == 0 || ((a == 0 || k == 0) && b == 1)) return 0;     \
@@ -247,7 +250,7 @@ int oracle_gemm_batched_##SUF(char ta, char tb, int m, int n, int k, const CT *a
                               CT *C, int ldc, long long ldc2, int batch)                \
 {                                                                                       \
     int rc = validate(0, ta, tb, m, n, k, alpha, alpha && O_CZERO(*alpha), beta, A,     \
-                      lda, lda2, B, ldb, ldb2, C, ldc, ldc2, batch, sizeof(CT));        \
+                      lda, lda2, B, ldb, ldb2, C, ldc, ldc2, batch, sizeof(CT), O_MAXDIM_CPLX);        \
     if (rc) return rc;                                                                  \
     CT a = *alpha, b = *beta;                                                           \
     if (m == 0 || n == 0 || batch == 0 || ((O_CZERO(a) || k == 0) && O_CONE(b)))        \
@@ -265,7 +268,7 @@ int oracle_gemm_batched_ptr_##SUF(char ta, char tb, int m, int n, int k,        
 {                                                                                       \
     int rc = validate(1, ta, tb, m, n, k, alpha, alpha && O_CZERO(*alpha), beta,        \
                       Aarray, lda, 0, Barray, ldb, 0, Carray, ldc, 0, batch,            \
-                      sizeof(CT));                                                      \
+                      sizeof(CT), O_MAXDIM_CPLX);                                                      \
     if (rc) return rc;                                                                  \
     CT a = *alpha, b = *beta;                                                           \
     if (m == 0 || n == 0 || batch == 0 || ((O_CZERO(a) || k == 0) && O_CONE(b)))        \

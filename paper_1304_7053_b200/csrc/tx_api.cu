@@ -156,13 +156,14 @@ static bool overlap(const void *p, long long np, const void *q, long long nq, si
 static int validate(bool ptr, char ta, char tb, int m, int n, int k, const void *alpha,
                     bool alpha_zero, const void *beta, const void *A, int lda, long long lda2,
                     const void *B, int ldb, long long ldb2, const void *C, int ldc,
-                    long long ldc2, int batch, size_t es)
+                    long long ldc2, int batch, size_t es, bool cplx)
 {
+    const int maxdim = cplx ? TX_MAX_DIM_CPLX : TX_MAX_DIM;
     if (!op_ok(ta)) return -1;
     if (!op_ok(tb)) return -2;
-    if (m < 0 || m > TX_MAX_DIM) return -3;
-    if (n < 0 || n > TX_MAX_DIM) return -4;
-    if (k < 0 || k > TX_MAX_DIM) return -5;
+    if (m < 0 || m > maxdim) return -3;
+    if (n < 0 || n > maxdim) return -4;
+    if (k < 0 || k > maxdim) return -5;
     if (!alpha) return -6;
     if (!beta) return ptr ? -11 : -13;
     const int rowsA = op_n(ta) ? m : k, colsA = op_n(ta) ? k : m;
@@ -245,6 +246,28 @@ bool encode_tma_rows(TmaDesc *d, const void *base, int es, int k, long long rows
 
 static int as_status(cudaError_t e) { return e == cudaSuccess ? 0 : (int)e; }
 
+// FP64 tensor-core (DMMA) instances for d / z: TX_DMMA=0 never, =1 always (A/B
+// measurements); unset: square AOT instances per tx_mma_table.inc, runtime-
+// specialised shapes by mma_jit_rule.
+int mma_mode()
+{
+    static const int mode = [] {
+        const char *v = getenv("TX_DMMA");
+        if (!v || !*v) return -1;
+        return v[0] == '0' ? 0 : 1;
+    }();
+    return mode;
+}
+
+// Runtime-specialised shapes (non-square, pointer arrays, padded layouts): the
+// tensor-core instance where measured faster (DMMA).
+bool mma_jit_rule(bool cplx, int m, int n, int k, bool ptr)
+{
+    (void)ptr;
+    const int mx = std::max(m, std::max(n, k));
+    return cplx && mx >= 13;
+}
+
 // Register-direct kernel for n <= 2 (TX_DIRECT=0 disables it: A/B measurements).
 static bool direct_enabled()
 {
@@ -268,7 +291,7 @@ static int gemm_strided(char ta, char tb, int m, int n, int k, const U *alpha, c
     using AT = Api<U>;
     using T = typename AT::T;
     const int rc = validate(false, ta, tb, m, n, k, alpha, alpha && AT::zero(*alpha), beta, A, lda,
-                            lda2, B, ldb, ldb2, C, ldc, ldc2, batch, sizeof(U));
+                            lda2, B, ldb, ldb2, C, ldc, ldc2, batch, sizeof(U), AT::cplx);
     if (rc) return rc;
     const U a = *alpha, b = *beta;
     if (m == 0 || n == 0 || batch == 0 || ((AT::zero(a) || k == 0) && AT::one(b))) {
@@ -375,7 +398,14 @@ static int gemm_strided(char ta, char tb, int m, int n, int k, const U *alpha, c
             q.A += SA * c0;
             q.B += SB * c0;
             q.C += SC * c0;
-            LaunchFn fn = (m == n && n == k && m <= 16) ? tab.bulk_sq[opa][opb][b0][m - 1] : nullptr;
+            LaunchFn fn = nullptr;
+            if (m == n && n == k && m <= 16) {
+                fn = tab.bulk_sq[opa][opb][b0][m - 1];
+                const int mode = mma_mode();
+                if (tab.bulk_mma[opa][opb][b0][m - 1] &&
+                    (mode == 1 || (mode < 0 && tab.mma_on[opa][opb][b0][m - 1])))
+                    fn = tab.bulk_mma[opa][opb][b0][m - 1];
+            }
             cudaError_t e = cudaErrorNotSupported;
             path = PATH_BULK;
             if (!fn) {  // no AOT instance for this shape: runtime-specialised instance
@@ -428,7 +458,7 @@ static int gemm_strided_dev(char ta, char tb, int m, int n, int k, const U *alph
     using AT = Api<U>;
     using T = typename AT::T;
     const int rc = validate(false, ta, tb, m, n, k, alpha, false, beta, A, lda, lda2, B, ldb,
-                            ldb2, C, ldc, ldc2, batch, sizeof(U));
+                            ldb2, C, ldc, ldc2, batch, sizeof(U), AT::cplx);
     if (rc) return rc;
     if (m == 0 || n == 0 || batch == 0) {
         t_last_path = PATH_NONE;
@@ -521,7 +551,7 @@ static int gemm_ptr_dev(char ta, char tb, int m, int n, int k, const U *alpha, c
     using AT = Api<U>;
     using T = typename AT::T;
     const int rc = validate(true, ta, tb, m, n, k, alpha, false, beta, Aa, lda, 0, Ba, ldb, 0, Ca,
-                            ldc, 0, batch, sizeof(U));
+                            ldc, 0, batch, sizeof(U), AT::cplx);
     if (rc) return rc;
     if (m == 0 || n == 0 || batch == 0) {
         t_last_path = PATH_NONE;
@@ -571,7 +601,7 @@ static int gemm_ptr(char ta, char tb, int m, int n, int k, const U *alpha, const
     using AT = Api<U>;
     using T = typename AT::T;
     const int rc = validate(true, ta, tb, m, n, k, alpha, alpha && AT::zero(*alpha), beta, Aa, lda,
-                            0, Ba, ldb, 0, Ca, ldc, 0, batch, sizeof(U));
+                            0, Ba, ldb, 0, Ca, ldc, 0, batch, sizeof(U), AT::cplx);
     if (rc) return rc;
     const U a = *alpha, b = *beta;
     if (m == 0 || n == 0 || batch == 0 || ((AT::zero(a) || k == 0) && AT::one(b))) {
@@ -652,7 +682,7 @@ static int gemm_hostio(char ta, char tb, int m, int n, int k, const U *alpha, co
 {
     using AT = Api<U>;
     int rc = validate(false, ta, tb, m, n, k, alpha, alpha && AT::zero(*alpha), beta, hA, lda,
-                      lda2, hB, ldb, ldb2, hC, ldc, ldc2, batch, sizeof(U));
+                      lda2, hB, ldb, ldb2, hC, ldc, ldc2, batch, sizeof(U), AT::cplx);
     if (rc) return rc;
     const U a = *alpha, b = *beta;
     const bool work = m > 0 && n > 0 && batch > 0;

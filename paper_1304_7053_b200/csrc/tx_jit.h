@@ -57,8 +57,14 @@ cudaError_t launch_jit(JitKind kind, Params<T> p, int opa, int opb, bool b0, cud
     const bool k128 = (p.k * (int)sizeof(T)) % 128 == 0;
     const bool asw_ok = swz_kind && !devab && opa != OP_N && k128;
     const bool bsw_ok = swz_kind && !devab && opb == OP_N && k128;
+    // FP64 tensor cores (mma_pair, one warp per pair) for d / z with m, n, k <= 16
+    const int mmode = mma_mode();
+    const bool mma = MmaOk<T>::value && !devab && !bcast && p.m <= 16 && p.n <= 16 &&
+                     p.k <= 16 &&
+                     (mmode == 1 || (mmode < 0 && mma_jit_rule(cplx, p.m, p.n, p.k, !gather ? false : kind != JIT_GATHER)));
     JitMap mp = jit_mapping((int)sizeof(T), cplx, p.m, p.n, p.k, opa, opb, b0,
-                            kind != JIT_BULK, asw_ok, bsw_ok);
+                            kind != JIT_BULK, asw_ok && !mma, bsw_ok && !mma);
+    if (mma) mp.ASW = mp.BSW = 0;  // the micro-tile mapping is unused
     constexpr int NT = NT_DEFAULT;
     char head[256];
     const char *kname = kind == JIT_BULK ? "bulk_kernel"
@@ -72,13 +78,16 @@ cudaError_t launch_jit(JitKind kind, Params<T> p, int opa, int opb, bool b0, cud
         expr += devab ? ", true" : ", false";
         expr += mp.ASW ? ", true" : ", false";
         expr += mp.BSW ? ", true" : ", false";
+        if (mma) expr += ", true";
     }
+    if (kind == JIT_BULK_PTR && mma) expr += ", true";
     const bool swz = kind == JIT_BULK && (mp.ASW || mp.BSW);
-    if (kind == JIT_BULK && (bcast || devab || swz)) {  // <..., BCAST, TRA, DEVAB, ASW, BSW>
+    if (kind == JIT_BULK && (bcast || devab || swz || mma)) {  // <..., BCAST, TRA, DEVAB, ASW, BSW[, MMA]>
         expr += ", " + std::to_string(bcast) + ", false";
         expr += devab ? ", true" : ", false";
         expr += mp.ASW ? ", true" : ", false";
         expr += mp.BSW ? ", true" : ", false";
+        if (mma) expr += ", true";
     }
     expr += ">";
     CUfunction f = jit_function(expr);
@@ -95,7 +104,7 @@ cudaError_t launch_jit(JitKind kind, Params<T> p, int opa, int opb, bool b0, cud
     }();
     Plan pl = plan_tiles(sizeof(T), p.m, p.n, p.k, b0, mp.RM, mp.RN, NT, p.batch, !gather,
                          gather ? GS : mp.S, kb, kind == JIT_BULK ? bcast : 0, 0, rows_cap,
-                         kind == JIT_BULK && two_ctas);
+                         kind == JIT_BULK && two_ctas, mma ? 32 : 0);
     if (swz) {
         // the 1024-byte alignment of the swizzled regions: shrink the tile until it fits
         const int es = (int)sizeof(T);

@@ -31,7 +31,7 @@ typedef unsigned long long uintptr_t;
 
 namespace tx {
 
-constexpr int TXK_MAX_DIM = 32;  // largest m, n, k (TX_MAX_DIM in include/txgemm.h)
+constexpr int TXK_MAX_DIM = 64;  // largest m, n, k (TX_MAX_DIM in include/txgemm.h)
 
 // A 128-byte TMA tensor map (the CUtensorMap blob, encoded on the host by
 // cuTensorMapEncodeTiled); used by the ASW bulk instances.
@@ -320,6 +320,153 @@ __device__ __forceinline__ void micro_tile(const T *__restrict__ a, const T *__r
     }
 }
 
+// --------------------------------------------------------------------------
+// FP64 tensor-core (DMMA) inner products: one WARP computes one whole C^p
+// (m, n <= 16: up to 2 x 2 tiles of 8 x 8) with mma.sync m8n8k4 f64.
+//
+// Measured on the B200 (tools/dmma_probe.py): D = A*B + C of m8n8k4 f64 is
+// exactly the chain of fused multiply-adds over k = 0, 1, 2, 3 in that order,
+// for every element (16384 / 16384, including inputs spread over 2^+-30), and
+// runs at the DFMA rate (37 TFlop/s).  So a k-step that covers 4 consecutive
+// terms of the ascending-l FMA chain of micro_tile reproduces that chain bit for
+// bit, with 1 instruction per 256 FMAs instead of 8 and the operands read from
+// shared memory once per warp instead of once per register micro-tile.
+//
+// Real (double): k-step s covers l = 4s .. 4s+3.
+// Complex (double2) in real form, interleaving (re, im) along k: k' = 2l + e,
+//   Cr = sum_k' A'[i][k'] B'[k'][j],  A'[2l+e] = (ar, sab*ai)[e], B'[2l+e] = (br, bi)[e]
+//   Ci = sum_k' A''[i][k'] B''[k'][j], A''[2l+e] = (ar, sa*ai)[e], B''[2l+e] = (sb*bi, br)[e]
+// -- exactly mac<CA,CB>'s two chains (acc.x: ar*br then sab*ai*bi; acc.y:
+// ar*(sb*bi) then (sa*ai)*br), sa/sb/sab the conjugation signs.  Rows, columns
+// and l past the matrix read as 0: fma(0, 0, acc) == acc (acc, started at +0,
+// is never -0 in round-to-nearest), so padding changes no bit.
+// Fragment layouts (probed): A 8x4 row: a = A[g][t]; B 4x8 col: b = B[t][g];
+// C 8x8: {c0, c1} = C[g][2t], C[g][2t+1]; g = lane / 4, t = lane % 4.
+// --------------------------------------------------------------------------
+__device__ __forceinline__ void dmma884(double &d0, double &d1, double a, double b)
+{
+    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+        : "+d"(d0), "+d"(d1)
+        : "d"(a), "d"(b));
+}
+
+template <class T> struct MmaOk { static constexpr bool value = false; };
+template <> struct MmaOk<double> { static constexpr bool value = true; };
+template <> struct MmaOk<double2> { static constexpr bool value = true; };
+
+// One C^p by the lanes of one warp.  a, b, cin: packed stored matrices in shared
+// memory; cout/ldo: destination.  MS, NS, KS <= 16, compile-time.
+template <class T, int MS, int NS, int KS, int OPA, int OPB, bool B0>
+__device__ __forceinline__ void mma_pair(const T *__restrict__ a, const T *__restrict__ b,
+                                         const T *__restrict__ cin, T *__restrict__ cout,
+                                         long long ldo, int lane, T alpha, T beta)
+{
+    static_assert(MmaOk<T>::value && MS > 0 && MS <= 16 && NS > 0 && NS <= 16 && KS > 0 && KS <= 16,
+                  "mma_pair: double / double2, sizes 1..16");
+    constexpr bool CPLX = same_t<T, double2>::value;
+    constexpr int RT = (MS + 7) / 8, CT = (NS + 7) / 8;
+    constexpr int KSTEPS = CPLX ? (2 * KS + 3) / 4 : (KS + 3) / 4;
+    const int g = lane >> 2, t = lane & 3;
+    double acc[RT][CT][CPLX ? 2 : 1][2];
+#pragma unroll
+    for (int r = 0; r < RT; ++r)
+#pragma unroll
+        for (int c = 0; c < CT; ++c)
+#pragma unroll
+            for (int h = 0; h < (CPLX ? 2 : 1); ++h) acc[r][c][h][0] = acc[r][c][h][1] = 0.0;
+
+    if constexpr (CPLX) {
+        constexpr bool CA = OPA == OP_C, CB = OPB == OP_C;
+        const int e = t & 1;
+        // lane-dependent signs of the odd (imaginary) k' entries
+        const bool neg_a1 = e && !(CA != CB);  // sab = -1 unless exactly one side conjugated
+        const bool neg_a2 = e && CA;           // sa
+        const bool neg_b2 = !e && CB;          // sb on the bi entry (even k' of B'')
+        const double2 *A2 = reinterpret_cast<const double2 *>(a);
+        const double2 *B2 = reinterpret_cast<const double2 *>(b);
+#pragma unroll
+        for (int s = 0; s < KSTEPS; ++s) {
+            const int l = 2 * s + (t >> 1);
+            double af[RT];
+#pragma unroll
+            for (int r = 0; r < RT; ++r) {
+                const int i = r * 8 + g;
+                double v = 0.0;
+                if (i < MS && l < KS) {
+                    const double *p = reinterpret_cast<const double *>(
+                        OPA == OP_N ? A2 + i + MS * l : A2 + l + KS * i);
+                    v = p[e];
+                }
+                af[r] = v;
+            }
+            double2 bf[CT];
+#pragma unroll
+            for (int c = 0; c < CT; ++c) {
+                const int j = c * 8 + g;
+                bf[c] = (j < NS && l < KS) ? (OPB == OP_N ? B2[l + KS * j] : B2[j + NS * l])
+                                           : make_double2(0.0, 0.0);
+            }
+#pragma unroll
+            for (int r = 0; r < RT; ++r) {
+                const double a1 = neg_a1 ? -af[r] : af[r];
+                const double a2 = neg_a2 ? -af[r] : af[r];
+#pragma unroll
+                for (int c = 0; c < CT; ++c) {
+                    const double b1 = e ? bf[c].y : bf[c].x;
+                    const double b2 = e ? bf[c].x : (neg_b2 ? -bf[c].y : bf[c].y);
+                    dmma884(acc[r][c][0][0], acc[r][c][0][1], a1, b1);
+                    dmma884(acc[r][c][1][0], acc[r][c][1][1], a2, b2);
+                }
+            }
+        }
+    } else {
+        const double *A1 = reinterpret_cast<const double *>(a);
+        const double *B1 = reinterpret_cast<const double *>(b);
+#pragma unroll
+        for (int s = 0; s < KSTEPS; ++s) {
+            const int l = 4 * s + t;
+            double af[RT], bf[CT];
+#pragma unroll
+            for (int r = 0; r < RT; ++r) {
+                const int i = r * 8 + g;
+                af[r] = (i < MS && l < KS) ? (OPA == OP_N ? A1[i + MS * l] : A1[l + KS * i]) : 0.0;
+            }
+#pragma unroll
+            for (int c = 0; c < CT; ++c) {
+                const int j = c * 8 + g;
+                bf[c] = (j < NS && l < KS) ? (OPB == OP_N ? B1[l + KS * j] : B1[j + NS * l]) : 0.0;
+            }
+#pragma unroll
+            for (int r = 0; r < RT; ++r)
+#pragma unroll
+                for (int c = 0; c < CT; ++c) dmma884(acc[r][c][0][0], acc[r][c][0][1], af[r], bf[c]);
+        }
+    }
+    // epilogue: the paper's axpby functors, as in micro_tile
+#pragma unroll
+    for (int r = 0; r < RT; ++r) {
+        const int i = r * 8 + g;
+        if (i >= MS) continue;
+#pragma unroll
+        for (int c = 0; c < CT; ++c)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int j = c * 8 + 2 * t + h;
+                if (j >= NS) continue;
+                T x;
+                if constexpr (CPLX) {
+                    x = make_double2(acc[r][c][0][h], acc[r][c][1][h]);
+                } else {
+                    x = acc[r][c][0][h];
+                }
+                T y;
+                if constexpr (B0) y = ax(alpha, x);
+                else y = axpby(alpha, x, beta, cin[i + MS * j]);
+                cout[i + ldo * j] = y;
+            }
+    }
+}
+
 // Threads -> (matrix q of the tile, row block, column block) work items.
 template <class MP>
 __device__ __forceinline__ void split_item(int sub, int RB, int CB, int &rb, int &cb)
@@ -379,10 +526,15 @@ __device__ __forceinline__ void scale_packed(T *c, long long elems, T beta, bool
 // with op N (p.tma_b, one row per stored column of B).  The swizzled regions
 // start on 1024-byte boundaries (the swizzle atom); the host caps P*m (P*n) at
 // 256 (the box height limit) and adds the alignment slack to the shared memory.
+// MMA (double / double2, square sizes <= 16, no BCAST/TRA/DEVAB/ASW/BSW): each
+// warp computes whole pairs with the FP64 tensor cores (mma_pair).
 template <class T, int MS, int NS, int KS, int OPA, int OPB, bool B0, class MP, int NT,
-          int BCAST = 0, bool TRA = false, bool DEVAB = false, bool ASW = false, bool BSW = false>
+          int BCAST = 0, bool TRA = false, bool DEVAB = false, bool ASW = false, bool BSW = false,
+          bool MMA = false>
 __global__ void __launch_bounds__(NT) bulk_kernel(const __grid_constant__ Params<T> p)
 {
+    static_assert(!MMA || (MmaOk<T>::value && BCAST == 0 && !TRA && !DEVAB && !ASW && !BSW &&
+                           MS > 0 && NS > 0 && KS > 0), "MMA");
     constexpr bool BA = (BCAST & 1) != 0, BB = (BCAST & 2) != 0;
     static_assert(!TRA || (OPA != OP_N && BCAST == 0 && MS > 0 && MP::VA == 1), "TRA");
     static_assert(!DEVAB || (!B0 && !TRA && BCAST == 0), "DEVAB");
@@ -525,6 +677,12 @@ __global__ void __launch_bounds__(NT) bulk_kernel(const __grid_constant__ Params
                     atr + q * (LDT * KS), sB + (BB ? 0 : q * SB), B0 ? nullptr : sC + q * SC,
                     gC + q * SC, m, rb, cb, q, m, n, k, p.alpha, p.beta);
             }
+        } else if constexpr (MMA) {
+            const int warp = tid >> 5, lane = tid & 31;
+            for (int q = warp; q < np; q += NT / 32)
+                mma_pair<T, MS, NS, KS, OPA, OPB, B0>(sA + q * SA, sB + q * SB,
+                                                      B0 ? nullptr : sC + q * SC, gC + q * SC, m,
+                                                      lane, alpha, beta);
         } else if (DEVAB && b0r) {  // run-time beta == 0: C is never read
             for (int w = tid; w < items; w += NT) {
                 const int q = w / TPM;
@@ -573,7 +731,8 @@ __global__ void __launch_bounds__(NT) bulk_kernel(const __grid_constant__ Params
 // mbarrier (its bytes are excluded from the expected count).
 // P <= 32 * PPL pairs per tile.
 // --------------------------------------------------------------------------
-template <class T, int MS, int NS, int KS, int OPA, int OPB, bool B0, class MP, int NT>
+template <class T, int MS, int NS, int KS, int OPA, int OPB, bool B0, class MP, int NT,
+          bool MMA = false>
 __global__ void __launch_bounds__(NT) bulk_ptr_kernel(const Params<T> p)
 {
     constexpr int PPL = 4;  // pointer triples per lane (P <= 128)
@@ -676,15 +835,22 @@ __global__ void __launch_bounds__(NT) bulk_ptr_kernel(const Params<T> p)
         const T *st = stage0 + (long long)(i % S) * stage_elems;
         const T *sA = st, *sB = st + P * SA, *sC = st + P * (SA + SB);
         mbar_wait(&bars[i % S], (i / S) & 1);
-        const int items = np * TPM;
-        for (int w = tid; w < items; w += NT) {
-            const int q = w / TPM;
-            int rb, cb;
-            split_item<MP>(w - q * TPM, RB, CB, rb, cb);
-            micro_tile<T, MS, NS, KS, OPA, OPB, B0, MP>(sA + q * SA, sB + q * SB,
-                                                        B0 ? nullptr : sC + q * SC,
-                                                        p.Cp[pair0 + q], p.ldc, rb, cb, q, m, n,
-                                                        k, p.alpha, p.beta);
+        if constexpr (MMA) {  // FP64 tensor cores: one warp per pair
+            for (int q = warp; q < np; q += NT / 32)
+                mma_pair<T, MS, NS, KS, OPA, OPB, B0>(sA + q * SA, sB + q * SB,
+                                                      B0 ? nullptr : sC + q * SC, p.Cp[pair0 + q],
+                                                      p.ldc, lane, p.alpha, p.beta);
+        } else {
+            const int items = np * TPM;
+            for (int w = tid; w < items; w += NT) {
+                const int q = w / TPM;
+                int rb, cb;
+                split_item<MP>(w - q * TPM, RB, CB, rb, cb);
+                micro_tile<T, MS, NS, KS, OPA, OPB, B0, MP>(sA + q * SA, sB + q * SB,
+                                                            B0 ? nullptr : sC + q * SC,
+                                                            p.Cp[pair0 + q], p.ldc, rb, cb, q, m,
+                                                            n, k, p.alpha, p.beta);
+            }
         }
         __syncthreads();
     }
@@ -711,9 +877,12 @@ constexpr int GS = 3;
 // the transposed reads of A are conflict-free at no extra cost.  BSWG: the same
 // for B with op N (its columns are the k-contiguous lines).
 template <class T, int MS, int NS, int KS, int OPA, int OPB, bool B0, class MP, int NT, bool PTR,
-          bool V16 = false, bool DEVAB = false, bool ASWG = false, bool BSWG = false>
+          bool V16 = false, bool DEVAB = false, bool ASWG = false, bool BSWG = false,
+          bool MMA = false>
 __global__ void __launch_bounds__(NT) gather_kernel(const Params<T> p)
 {
+    static_assert(!MMA || (MmaOk<T>::value && !DEVAB && !ASWG && !BSWG && MS > 0 && NS > 0 &&
+                           KS > 0), "MMA");
     static_assert(!DEVAB || !B0, "DEVAB");
     static_assert(!ASWG || (OPA != OP_N && KS > 0 && (KS * sizeof(T)) % 128 == 0 && !DEVAB), "ASWG");
     static_assert(!BSWG || (OPB == OP_N && KS > 0 && (KS * sizeof(T)) % 128 == 0 && !DEVAB), "BSWG");
@@ -864,7 +1033,17 @@ __global__ void __launch_bounds__(NT) gather_kernel(const Params<T> p)
         const int np = (int)min((long long)P, p.batch - pair0);
         const T *st = stage0 + (long long)(i % GS) * stage_elems;
         const T *sA = st, *sB = st + P * SA, *sC = st + P * (SA + SB);
-        const int items = np * TPM;
+        const int items = MMA ? 0 : np * TPM;
+        if constexpr (MMA) {  // FP64 tensor cores: one warp per pair
+            const int warp = tid >> 5, lane = tid & 31;
+            for (int q = warp; q < np; q += NT / 32) {
+                T *cout = PTR ? const_cast<T *>(ptab[(i % GS) * 3 * P + 2 * P + q])
+                              : p.C + (pair0 + q) * p.ldc2;
+                mma_pair<T, MS, NS, KS, OPA, OPB, B0>(sA + q * SA, sB + q * SB,
+                                                      B0 ? nullptr : sC + q * SC, cout, p.ldc,
+                                                      lane, alpha, beta);
+            }
+        }
         for (int w = tid; w < items; w += NT) {
             const int q = w / TPM;
             int rb, cb;

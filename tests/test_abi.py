@@ -57,7 +57,7 @@ def _vec(**kw):
 
 
 BAD = [
-    dict(ta="x"), dict(tb="?"), dict(m=-1), dict(m=33), dict(n=99), dict(k=-3),
+    dict(ta="x"), dict(tb="?"), dict(m=-1), dict(m=65), dict(n=99), dict(k=-3),
     dict(alpha_ptr=False), dict(beta_ptr=False), dict(lda=3), dict(ta="T", k=5, lda=4),
     dict(ldb=2), dict(ldc=1), dict(lda2=-5), dict(ldb2=-1), dict(ldc2=15), dict(batch=-2),
     dict(A=None), dict(B=None), dict(C=None), dict(C=FAKE + 8),  # C overlaps A
@@ -164,3 +164,18 @@ def test_prepare_argument_errors():
     assert tx.prepare("s", "N", "N", 4, 4, 99) == -6
     assert tx.prepare("s", "N", "N", 4, 4, 4, layout=7) == -8
     assert tx.prepare("s", "N", "N", 0, 4, 4) == 0  # quick return: nothing to build
+
+
+def test_complex_size_limit():
+    """m, n, k up to 64 for s/d but 32 for c/z (include/txgemm.h TX_MAX_DIM_CPLX)."""
+    f = tx.tx_gemm_batched
+    for kind in "cz":
+        assert f(kind, "N", "N", 33, 4, 4, 1, FAKE, 33, 132, FAKE + (1 << 20), 4, 16, 0,
+                 FAKE + (2 << 20), 33, 132, 3, stream=0) == -3
+        assert f(kind, "N", "N", 4, 33, 4, 1, FAKE, 4, 16, FAKE + (1 << 20), 4, 132, 0,
+                 FAKE + (2 << 20), 4, 132, 3, stream=0) == -4
+        assert f(kind, "N", "N", 4, 4, 33, 1, FAKE, 4, 132, FAKE + (1 << 20), 33, 132, 0,
+                 FAKE + (2 << 20), 4, 16, 3, stream=0) == -5
+    for kind in "sd":  # 65 is past the real limit
+        assert f(kind, "N", "N", 65, 4, 4, 1, FAKE, 65, 260, FAKE + (1 << 20), 4, 16, 0,
+                 FAKE + (2 << 20), 65, 260, 3, stream=0) == -3

@@ -15,9 +15,9 @@ OPS = st.sampled_from(list("nNtTcCxq "))
 
 
 @settings(max_examples=400, deadline=None)
-@given(kind=st.sampled_from("sdcz"), ta=OPS, tb=OPS, m=st.integers(-2, 34), n=st.integers(-2, 34),
-       k=st.integers(-2, 34), lda=st.integers(-1, 36), ldb=st.integers(-1, 36),
-       ldc=st.integers(-1, 36), lda2=st.integers(-3, 1200), ldb2=st.integers(-3, 1200),
+@given(kind=st.sampled_from("sdcz"), ta=OPS, tb=OPS, m=st.integers(-2, 66), n=st.integers(-2, 66),
+       k=st.integers(-2, 66), lda=st.integers(-1, 68), ldb=st.integers(-1, 68),
+       ldc=st.integers(-1, 68), lda2=st.integers(-3, 1200), ldb2=st.integers(-3, 1200),
        ldc2=st.integers(-3, 1200), batch=st.integers(-2, 5), alpha=st.sampled_from([0.0, 1.0, 2.5]),
        beta=st.sampled_from([0.0, 1.0, -0.5]), a_null=st.booleans(), b_null=st.booleans(),
        c_null=st.booleans(), alpha_ptr=st.booleans(), beta_ptr=st.booleans(),

@@ -546,12 +546,16 @@ def test_cuda_graph_capture_and_replay_with_device_scalars():
 
 # --------------------------------------------------- sizes beyond 16 (NEXT-4)
 @pytest.mark.parametrize("kind", "sdcz")
-@pytest.mark.parametrize("mnk", [(17, 17, 17), (24, 24, 24), (32, 32, 32), (32, 8, 20), (3, 32, 29)],
+@pytest.mark.parametrize("mnk", [(17, 17, 17), (24, 24, 24), (32, 32, 32), (32, 8, 20), (3, 32, 29),
+                                 (48, 48, 48), (64, 64, 64), (64, 17, 40), (33, 64, 9)],
                          ids=lambda t: "x".join(map(str, t)))
 def test_sizes_beyond_16(kind, mnk):
-    """m, n, k up to 32 ("easily extended to larger sizes"): packed
-    (runtime-specialised bulk), padded (gather) and both epilogues."""
+    """m, n, k up to 64 for s/d, 32 for c/z ("easily extended to larger sizes",
+    PAPER.md:33-34): packed (runtime-specialised bulk), padded (gather) and both
+    epilogues."""
     m, n, k = mnk
+    if kind in "cz" and max(mnk) > 32:
+        pytest.skip("c/z sizes stop at 32 (TX_MAX_DIM_CPLX)")
     ops = [("N", "N"), ("T", "N"), ("N", "C" if kind in "cz" else "T")]
     for ta, tb in ops:
         for general in (False, True):
@@ -566,7 +570,7 @@ def test_sizes_beyond_16(kind, mnk):
 
 
 @pytest.mark.parametrize("kind", "sdcz")
-@pytest.mark.parametrize("mnk", [(32, 32, 32), (24, 8, 32), (5, 30, 32)],
+@pytest.mark.parametrize("mnk", [(32, 32, 32), (24, 8, 32), (5, 30, 32), (64, 64, 64), (48, 40, 16)],
                          ids=lambda t: "x".join(map(str, t)))
 def test_pointer_arrays_beyond_16(kind, mnk):
     """Pointer arrays at sizes 17-32 with k * sizeof(T) a multiple of 128 B (swizzled
@@ -575,6 +579,8 @@ def test_pointer_arrays_beyond_16(kind, mnk):
     import torch
 
     m, n, k = mnk
+    if kind in "cz" and max(mnk) > 32:
+        pytest.skip("c/z sizes stop at 32 (TX_MAX_DIM_CPLX)")
     for ta, tb in (("N", "N"), ("T", "N"), ("C" if kind in "cz" else "T", "T")):
         A, B, C = random_case(kind, m, n, k, 129, ta, tb, seed=12, tag="ptrbig")
         alpha, beta = _ab(kind, f"ptrbig{m}{n}{k}")
@@ -678,3 +684,36 @@ def test_direct_tiny_matrices(kind, n):
                 assert tx.tx_gemm_batched_ptr(kind, ta, tb, n, n, n, alpha, pa, n, pb, n, beta, pc,
                                               n, batch) == 0
                 assert np.array_equal(dC.cpu().numpy().view(np.uint8), got.view(np.uint8))
+
+
+# -------------------------------------------- FP64 tensor cores (DMMA), d / z
+@pytest.mark.parametrize("kind", "dz")
+@pytest.mark.parametrize("n", range(1, 17))
+def test_dmma_square_instances_bitwise_vs_fma_path(kind, n):
+    """Square d/z instances run the FP64 tensor cores (mma.sync m8n8k4, one warp per
+    pair); the generic AOT pointer-array kernel (runtime specialisation off) runs the
+    FMA micro-tiles.  DMMA is the same fused FMA chain over k (tools/dmma_probe.py),
+    so the two are bitwise equal; both match the oracle.  Ragged batches, every op
+    pair, both epilogues."""
+    import torch
+    from paper_1304_7053_b200 import binding
+
+    for ta, tb in ops_for(kind):
+        for general in (False, True):
+            err, path, (A, B, C, alpha, beta, got, ref) = _case(kind, n, n, n, 999, ta, tb, general,
+                                                                f"dmma{n}")
+            dA, _ = to_dev(A)
+            dB, _ = to_dev(B)
+            dC, _ = to_dev(C)
+            es = dA.element_size()
+            pa = torch.tensor(A.offsets() * es + dA.data_ptr(), device="cuda")
+            pb = torch.tensor(B.offsets() * es + dB.data_ptr(), device="cuda")
+            pc = torch.tensor(C.offsets() * es + dC.data_ptr(), device="cuda")
+            prev = binding.set_jit(False)
+            try:
+                assert tx.tx_gemm_batched_ptr(kind, ta, tb, n, n, n, alpha, pa, A.ld, pb, B.ld,
+                                              beta, pc, C.ld, C.batch) == 0
+                assert not binding.last_path_jit()
+            finally:
+                binding.set_jit(prev)
+            assert np.array_equal(dC.cpu().numpy().view(np.uint8), got.view(np.uint8)), (n, ta, tb)

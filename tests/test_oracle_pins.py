@@ -424,8 +424,11 @@ VALIDATION = [
     ("transa", {"ta": "x"}, -1),
     ("transb", {"tb": "Q"}, -2),
     ("m<0", {"m": -1}, -3),
-    ("m>32", {"m": 33}, -3),
-    ("n>32", {"n": 33}, -4),
+    ("m>64", {"m": 65}, -3),
+    ("n>64", {"n": 65}, -4),
+    ("m=64 valid (real)", {"m": 64, "lda": 64, "ldc": 64, "ldc2": 256}, 0),
+    ("m>32 complex", {"kind": "z", "m": 33, "lda": 33, "ldc": 33, "ldc2": 132}, -3),
+    ("k>32 complex", {"kind": "c", "k": 33}, -5),
     ("m=17 valid", {"m": 17, "lda": 17, "ldc": 17, "ldc2": 68}, 0),
     ("k<0", {"k": -2}, -5),
     ("alpha NULL", {"alpha_ptr": False}, -6),
