@@ -265,7 +265,7 @@ bool mma_jit_rule(bool cplx, int m, int n, int k, bool ptr)
 {
     (void)ptr;
     const int mx = std::max(m, std::max(n, k));
-    return cplx && mx >= 13;
+    return cplx ? mx >= 13 : mx >= 17;
 }
 
 // Register-direct kernel for n <= 2 (TX_DIRECT=0 disables it: A/B measurements).

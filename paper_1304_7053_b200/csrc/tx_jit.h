@@ -57,11 +57,11 @@ cudaError_t launch_jit(JitKind kind, Params<T> p, int opa, int opb, bool b0, cud
     const bool k128 = (p.k * (int)sizeof(T)) % 128 == 0;
     const bool asw_ok = swz_kind && !devab && opa != OP_N && k128;
     const bool bsw_ok = swz_kind && !devab && opb == OP_N && k128;
-    // FP64 tensor cores (mma_pair, one warp per pair) for d / z with m, n, k <= 16
+    // FP64 tensor cores (mma_item, one warp per macro-tile) for d / z
     const int mmode = mma_mode();
-    const bool mma = MmaOk<T>::value && !devab && !bcast && p.m <= 16 && p.n <= 16 &&
-                     p.k <= 16 &&
-                     (mmode == 1 || (mmode < 0 && mma_jit_rule(cplx, p.m, p.n, p.k, !gather ? false : kind != JIT_GATHER)));
+    const bool mma = MmaOk<T>::value && !devab && !bcast &&
+                     (mmode == 1 || (mmode < 0 && mma_jit_rule(cplx, p.m, p.n, p.k,
+                                                               kind != JIT_BULK && kind != JIT_GATHER)));
     JitMap mp = jit_mapping((int)sizeof(T), cplx, p.m, p.n, p.k, opa, opb, b0,
                             kind != JIT_BULK, asw_ok && !mma, bsw_ok && !mma);
     if (mma) mp.ASW = mp.BSW = 0;  // the micro-tile mapping is unused
@@ -104,7 +104,7 @@ cudaError_t launch_jit(JitKind kind, Params<T> p, int opa, int opb, bool b0, cud
     }();
     Plan pl = plan_tiles(sizeof(T), p.m, p.n, p.k, b0, mp.RM, mp.RN, NT, p.batch, !gather,
                          gather ? GS : mp.S, kb, kind == JIT_BULK ? bcast : 0, 0, rows_cap,
-                         kind == JIT_BULK && two_ctas, mma ? 32 : 0);
+                         kind == JIT_BULK && two_ctas, mma ? 32 * mma_items(cplx, p.m, p.n) : 0);
     if (swz) {
         // the 1024-byte alignment of the swizzled regions: shrink the tile until it fits
         const int es = (int)sizeof(T);
@@ -142,6 +142,7 @@ cudaError_t launch_jit(JitKind kind, Params<T> p, int opa, int opb, bool b0, cud
         const int SA = p.m * p.k, SB = p.k * p.n, SC = p.m * p.n;
         pl.smem = pl.S * 128 * (SA + SB + (b0 ? 0 : SC)) * (int)sizeof(T) + 8 * pl.S;
     }
+    if (kind == JIT_BULK_PTR) pl.smem += pl.S * pl.P * 8;  // the C-pointer slots
     p.P = pl.P;
     p.S = pl.S;
     p.ntiles = pl.ntiles;

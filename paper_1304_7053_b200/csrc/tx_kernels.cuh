@@ -321,8 +321,8 @@ __device__ __forceinline__ void micro_tile(const T *__restrict__ a, const T *__r
 }
 
 // --------------------------------------------------------------------------
-// FP64 tensor-core (DMMA) inner products: one WARP computes one whole C^p
-// (m, n <= 16: up to 2 x 2 tiles of 8 x 8) with mma.sync m8n8k4 f64.
+// FP64 tensor-core (DMMA) inner products: one WARP computes a macro-tile of C^p
+// (RT x CT tiles of 8 x 8; the whole C^p when m, n <= 16) with mma.sync m8n8k4 f64.
 //
 // Measured on the B200 (tools/dmma_probe.py): D = A*B + C of m8n8k4 f64 is
 // exactly the chain of fused multiply-adds over k = 0, 1, 2, 3 in that order,
@@ -354,19 +354,39 @@ template <class T> struct MmaOk { static constexpr bool value = false; };
 template <> struct MmaOk<double> { static constexpr bool value = true; };
 template <> struct MmaOk<double2> { static constexpr bool value = true; };
 
-// One C^p by the lanes of one warp.  a, b, cin: packed stored matrices in shared
-// memory; cout/ldo: destination.  MS, NS, KS <= 16, compile-time.
+// Warp macro-tile shape of the tensor-core path: RT x CT tiles of 8 x 8 (accumulators
+// per lane: 2 * RT * CT doubles, twice that for complex), and the number of
+// macro-tiles (warp work items) per matrix.
+template <class T, int MS, int NS>
+struct MmaShape {
+    static constexpr bool CPLX = same_t<T, double2>::value;
+    static constexpr int RT = (MS + 7) / 8 < 2 ? (MS + 7) / 8 : 2;
+    static constexpr int CT_MAX = CPLX ? 2 : 4;
+    static constexpr int CT = (NS + 7) / 8 < CT_MAX ? (NS + 7) / 8 : CT_MAX;
+    static constexpr int MR = (MS + 8 * RT - 1) / (8 * RT);  // macro-tiles down the rows
+    static constexpr int MC = (NS + 8 * CT - 1) / (8 * CT);  // ... and across the columns
+    static constexpr int ITEMS = MR * MC;                    // warp items per matrix
+};
+
+// One macro-tile (item `it` of MmaShape::ITEMS) of C^p by the lanes of one warp.
+// a, b, cin: packed stored matrices in shared memory; cout/ldo: destination.
+// MS, NS, KS compile-time: <= 64 for double, <= 32 for double2.
 template <class T, int MS, int NS, int KS, int OPA, int OPB, bool B0>
-__device__ __forceinline__ void mma_pair(const T *__restrict__ a, const T *__restrict__ b,
+__device__ __forceinline__ void mma_item(const T *__restrict__ a, const T *__restrict__ b,
                                          const T *__restrict__ cin, T *__restrict__ cout,
-                                         long long ldo, int lane, T alpha, T beta)
+                                         long long ldo, int it, int lane, T alpha, T beta)
 {
-    static_assert(MmaOk<T>::value && MS > 0 && MS <= 16 && NS > 0 && NS <= 16 && KS > 0 && KS <= 16,
-                  "mma_pair: double / double2, sizes 1..16");
-    constexpr bool CPLX = same_t<T, double2>::value;
-    constexpr int RT = (MS + 7) / 8, CT = (NS + 7) / 8;
+    static_assert(MmaOk<T>::value && MS > 0 && NS > 0 && KS > 0 &&
+                      MS <= (same_t<T, double2>::value ? 32 : 64) &&
+                      NS <= (same_t<T, double2>::value ? 32 : 64) &&
+                      KS <= (same_t<T, double2>::value ? 32 : 64),
+                  "mma_item: double (sizes <= 64) / double2 (sizes <= 32)");
+    using SH = MmaShape<T, MS, NS>;
+    constexpr bool CPLX = SH::CPLX;
+    constexpr int RT = SH::RT, CT = SH::CT;
     constexpr int KSTEPS = CPLX ? (2 * KS + 3) / 4 : (KS + 3) / 4;
     const int g = lane >> 2, t = lane & 3;
+    const int i0 = (it % SH::MR) * 8 * RT, j0 = (it / SH::MR) * 8 * CT;
     double acc[RT][CT][CPLX ? 2 : 1][2];
 #pragma unroll
     for (int r = 0; r < RT; ++r)
@@ -384,13 +404,13 @@ __device__ __forceinline__ void mma_pair(const T *__restrict__ a, const T *__res
         const bool neg_b2 = !e && CB;          // sb on the bi entry (even k' of B'')
         const double2 *A2 = reinterpret_cast<const double2 *>(a);
         const double2 *B2 = reinterpret_cast<const double2 *>(b);
-#pragma unroll
+#pragma unroll 4
         for (int s = 0; s < KSTEPS; ++s) {
             const int l = 2 * s + (t >> 1);
             double af[RT];
 #pragma unroll
             for (int r = 0; r < RT; ++r) {
-                const int i = r * 8 + g;
+                const int i = i0 + r * 8 + g;
                 double v = 0.0;
                 if (i < MS && l < KS) {
                     const double *p = reinterpret_cast<const double *>(
@@ -402,7 +422,7 @@ __device__ __forceinline__ void mma_pair(const T *__restrict__ a, const T *__res
             double2 bf[CT];
 #pragma unroll
             for (int c = 0; c < CT; ++c) {
-                const int j = c * 8 + g;
+                const int j = j0 + c * 8 + g;
                 bf[c] = (j < NS && l < KS) ? (OPB == OP_N ? B2[l + KS * j] : B2[j + NS * l])
                                            : make_double2(0.0, 0.0);
             }
@@ -422,18 +442,18 @@ __device__ __forceinline__ void mma_pair(const T *__restrict__ a, const T *__res
     } else {
         const double *A1 = reinterpret_cast<const double *>(a);
         const double *B1 = reinterpret_cast<const double *>(b);
-#pragma unroll
+#pragma unroll 4
         for (int s = 0; s < KSTEPS; ++s) {
             const int l = 4 * s + t;
             double af[RT], bf[CT];
 #pragma unroll
             for (int r = 0; r < RT; ++r) {
-                const int i = r * 8 + g;
+                const int i = i0 + r * 8 + g;
                 af[r] = (i < MS && l < KS) ? (OPA == OP_N ? A1[i + MS * l] : A1[l + KS * i]) : 0.0;
             }
 #pragma unroll
             for (int c = 0; c < CT; ++c) {
-                const int j = c * 8 + g;
+                const int j = j0 + c * 8 + g;
                 bf[c] = (j < NS && l < KS) ? (OPB == OP_N ? B1[l + KS * j] : B1[j + NS * l]) : 0.0;
             }
 #pragma unroll
@@ -445,13 +465,13 @@ __device__ __forceinline__ void mma_pair(const T *__restrict__ a, const T *__res
     // epilogue: the paper's axpby functors, as in micro_tile
 #pragma unroll
     for (int r = 0; r < RT; ++r) {
-        const int i = r * 8 + g;
+        const int i = i0 + r * 8 + g;
         if (i >= MS) continue;
 #pragma unroll
         for (int c = 0; c < CT; ++c)
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
-                const int j = c * 8 + 2 * t + h;
+                const int j = j0 + c * 8 + 2 * t + h;
                 if (j >= NS) continue;
                 T x;
                 if constexpr (CPLX) {
@@ -527,7 +547,7 @@ __device__ __forceinline__ void scale_packed(T *c, long long elems, T beta, bool
 // start on 1024-byte boundaries (the swizzle atom); the host caps P*m (P*n) at
 // 256 (the box height limit) and adds the alignment slack to the shared memory.
 // MMA (double / double2, square sizes <= 16, no BCAST/TRA/DEVAB/ASW/BSW): each
-// warp computes whole pairs with the FP64 tensor cores (mma_pair).
+// warp computes warp macro-tiles with the FP64 tensor cores (mma_item).
 template <class T, int MS, int NS, int KS, int OPA, int OPB, bool B0, class MP, int NT,
           int BCAST = 0, bool TRA = false, bool DEVAB = false, bool ASW = false, bool BSW = false,
           bool MMA = false>
@@ -679,10 +699,13 @@ __global__ void __launch_bounds__(NT) bulk_kernel(const __grid_constant__ Params
             }
         } else if constexpr (MMA) {
             const int warp = tid >> 5, lane = tid & 31;
-            for (int q = warp; q < np; q += NT / 32)
-                mma_pair<T, MS, NS, KS, OPA, OPB, B0>(sA + q * SA, sB + q * SB,
+            constexpr int IT = MmaShape<T, (MS > 0 ? MS : 1), (NS > 0 ? NS : 1)>::ITEMS;
+            for (int w = warp; w < np * IT; w += NT / 32) {
+                const int q = w / IT;
+                mma_item<T, MS, NS, KS, OPA, OPB, B0>(sA + q * SA, sB + q * SB,
                                                       B0 ? nullptr : sC + q * SC, gC + q * SC, m,
-                                                      lane, alpha, beta);
+                                                      w - q * IT, lane, alpha, beta);
+            }
         } else if (DEVAB && b0r) {  // run-time beta == 0: C is never read
             for (int w = tid; w < items; w += NT) {
                 const int q = w / TPM;
@@ -745,6 +768,9 @@ __global__ void __launch_bounds__(NT) bulk_ptr_kernel(const Params<T> p)
     const int stage_elems = P * (SA + SB + (B0 ? 0 : SC));
     T *stage0 = reinterpret_cast<T *>(smem_raw);
     uint64_t *bars = reinterpret_cast<uint64_t *>(stage0 + (long long)S * stage_elems);
+    // the tile's C pointers, one slot per stage: written by warp 0 with the copies,
+    // read by every thread's epilogue (no dependent global load in the compute loop)
+    T **cptr = reinterpret_cast<T **>(bars + S);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int G = gridDim.x;
     const int my_tiles = (p.ntiles - (int)blockIdx.x + G - 1) / G;
@@ -767,7 +793,7 @@ __global__ void __launch_bounds__(NT) bulk_ptr_kernel(const Params<T> p)
             const bool ok = i < my_tiles && lane + 32 * r < P && q < p.batch;
             pa[r] = ok ? p.Ap[q] : nullptr;
             pb[r] = ok ? p.Bp[q] : nullptr;
-            pc[r] = (ok && !B0) ? (const T *)p.Cp[q] : nullptr;
+            pc[r] = ok ? (const T *)p.Cp[q] : nullptr;
         }
     };
     auto issue = [&](int i) {  // warp 0: copies of local tile i into stage i % S
@@ -778,6 +804,7 @@ __global__ void __launch_bounds__(NT) bulk_ptr_kernel(const Params<T> p)
         uint32_t mine = 0;
 #pragma unroll
         for (int r = 0; r < PPL; ++r) {
+            if (lane + 32 * r < P) cptr[(i % S) * P + lane + 32 * r] = const_cast<T *>(pc[r]);
             if (pa[r] && (((uintptr_t)pa[r] & 15) == 0)) mine += ba;
             if (pb[r] && (((uintptr_t)pb[r] & 15) == 0)) mine += bb;
             if (!B0 && pc[r] && (((uintptr_t)pc[r] & 15) == 0)) mine += bc;
@@ -835,11 +862,15 @@ __global__ void __launch_bounds__(NT) bulk_ptr_kernel(const Params<T> p)
         const T *st = stage0 + (long long)(i % S) * stage_elems;
         const T *sA = st, *sB = st + P * SA, *sC = st + P * (SA + SB);
         mbar_wait(&bars[i % S], (i / S) & 1);
-        if constexpr (MMA) {  // FP64 tensor cores: one warp per pair
-            for (int q = warp; q < np; q += NT / 32)
-                mma_pair<T, MS, NS, KS, OPA, OPB, B0>(sA + q * SA, sB + q * SB,
-                                                      B0 ? nullptr : sC + q * SC, p.Cp[pair0 + q],
-                                                      p.ldc, lane, p.alpha, p.beta);
+        if constexpr (MMA) {  // FP64 tensor cores: one warp per macro-tile
+            constexpr int IT = MmaShape<T, (MS > 0 ? MS : 1), (NS > 0 ? NS : 1)>::ITEMS;
+            for (int w = warp; w < np * IT; w += NT / 32) {
+                const int q = w / IT;
+                mma_item<T, MS, NS, KS, OPA, OPB, B0>(sA + q * SA, sB + q * SB,
+                                                      B0 ? nullptr : sC + q * SC,
+                                                      cptr[(i % S) * P + q], p.ldc, w - q * IT,
+                                                      lane, p.alpha, p.beta);
+            }
         } else {
             const int items = np * TPM;
             for (int w = tid; w < items; w += NT) {
@@ -848,7 +879,7 @@ __global__ void __launch_bounds__(NT) bulk_ptr_kernel(const Params<T> p)
                 split_item<MP>(w - q * TPM, RB, CB, rb, cb);
                 micro_tile<T, MS, NS, KS, OPA, OPB, B0, MP>(sA + q * SA, sB + q * SB,
                                                             B0 ? nullptr : sC + q * SC,
-                                                            p.Cp[pair0 + q], p.ldc, rb, cb, q, m,
+                                                            cptr[(i % S) * P + q], p.ldc, rb, cb, q, m,
                                                             n, k, p.alpha, p.beta);
             }
         }
@@ -861,7 +892,7 @@ __global__ void __launch_bounds__(NT) bulk_ptr_kernel(const Params<T> p)
 // into a GS-stage ring (packed stage layout identical to the bulk kernel's), C
 // written from registers at its true address.
 // --------------------------------------------------------------------------
-constexpr int GS = 3;
+constexpr int GS = 3;  // gather ring depth (2 when three stages of one tile do not fit)
 
 // V16: matrices are packed (ld = rows) with byte sizes that are multiples of 16;
 // they are moved in 16-byte chunks (a chunk whose source is not 16-byte aligned
@@ -893,10 +924,11 @@ __global__ void __launch_bounds__(NT) gather_kernel(const Params<T> p)
     const int rowsA = (OPA == OP_N) ? m : k;
     const int rowsB = (OPB == OP_N) ? k : n;
     const int P = p.P;
+    const int gs = p.S;  // ring depth (3, or 2 when three stages of the tile do not fit)
     const int stage_elems = P * (SA + SB + (B0 ? 0 : SC));
     T *stage0 = reinterpret_cast<T *>(smem_raw);
     const T **ptab = reinterpret_cast<const T **>(
-        smem_raw + (((long long)GS * stage_elems * sizeof(T) + 15) & ~15ll));
+        smem_raw + (((long long)gs * stage_elems * sizeof(T) + 15) & ~15ll));
     const int tid = threadIdx.x;
     const int G = gridDim.x;
     const int my_tiles = (p.ntiles - (int)blockIdx.x + G - 1) / G;
@@ -925,7 +957,7 @@ __global__ void __launch_bounds__(NT) gather_kernel(const Params<T> p)
         }
     };
     auto store_regs = [&](int j) {
-        const int slot = j % GS;
+        const int slot = j % gs;
 #pragma unroll
         for (int t = 0; t < PR; ++t) {
             const int idx = tid + t * NT;
@@ -934,7 +966,7 @@ __global__ void __launch_bounds__(NT) gather_kernel(const Params<T> p)
     };
     auto ptr_of = [&](int tile, int which, int q, const T *base, long long ld2,
                       long long pair0) -> const T * {
-        if constexpr (PTR) return ptab[(tile % GS) * 3 * P + which * P + q];
+        if constexpr (PTR) return ptab[(tile % gs) * 3 * P + which * P + q];
         else return base + (pair0 + q) * ld2;
     };
 
@@ -976,7 +1008,7 @@ __global__ void __launch_bounds__(NT) gather_kernel(const Params<T> p)
     auto issue = [&](int i) {
         const long long pair0 = (blockIdx.x + (long long)i * G) * P;
         const int np = (int)min((long long)P, p.batch - pair0);
-        T *st = stage0 + (long long)(i % GS) * stage_elems;
+        T *st = stage0 + (long long)(i % gs) * stage_elems;
         if constexpr (V16) {
             chunks16(i, 0, st, SA, np, pair0, p.A, p.lda2);
             chunks16(i, 1, st + P * SA, SB, np, pair0, p.B, p.ldb2);
@@ -1011,44 +1043,46 @@ __global__ void __launch_bounds__(NT) gather_kernel(const Params<T> p)
         }
     }
     if constexpr (PTR) {
-        for (int j = 0; j < GS; ++j) {
+        for (int j = 0; j < gs; ++j) {
             load_regs(j);
             store_regs(j);
         }
-        load_regs(GS);
+        load_regs(gs);
         __syncthreads();
     }
-    for (int i = 0; i < GS - 1; ++i) {
+    for (int i = 0; i < gs - 1; ++i) {
         if (i < my_tiles) issue(i);
         cp_async_commit();
     }
     const int RB = (m + MP::RM - 1) / MP::RM, CB = (n + MP::RN - 1) / MP::RN;
     const int TPM = RB * CB;
     for (int i = 0; i < my_tiles; ++i) {
-        if (i + GS - 1 < my_tiles) issue(i + GS - 1);
+        if (i + gs - 1 < my_tiles) issue(i + gs - 1);
         cp_async_commit();
-        cp_async_wait<GS - 1>();
+        if (gs == 3) cp_async_wait<2>(); else cp_async_wait<1>();
         __syncthreads();
         const long long pair0 = (blockIdx.x + (long long)i * G) * P;
         const int np = (int)min((long long)P, p.batch - pair0);
-        const T *st = stage0 + (long long)(i % GS) * stage_elems;
+        const T *st = stage0 + (long long)(i % gs) * stage_elems;
         const T *sA = st, *sB = st + P * SA, *sC = st + P * (SA + SB);
         const int items = MMA ? 0 : np * TPM;
-        if constexpr (MMA) {  // FP64 tensor cores: one warp per pair
+        if constexpr (MMA) {  // FP64 tensor cores: one warp per macro-tile
             const int warp = tid >> 5, lane = tid & 31;
-            for (int q = warp; q < np; q += NT / 32) {
-                T *cout = PTR ? const_cast<T *>(ptab[(i % GS) * 3 * P + 2 * P + q])
+            constexpr int IT = MmaShape<T, (MS > 0 ? MS : 1), (NS > 0 ? NS : 1)>::ITEMS;
+            for (int w = warp; w < np * IT; w += NT / 32) {
+                const int q = w / IT;
+                T *cout = PTR ? const_cast<T *>(ptab[(i % gs) * 3 * P + 2 * P + q])
                               : p.C + (pair0 + q) * p.ldc2;
-                mma_pair<T, MS, NS, KS, OPA, OPB, B0>(sA + q * SA, sB + q * SB,
+                mma_item<T, MS, NS, KS, OPA, OPB, B0>(sA + q * SA, sB + q * SB,
                                                       B0 ? nullptr : sC + q * SC, cout, p.ldc,
-                                                      lane, alpha, beta);
+                                                      w - q * IT, lane, alpha, beta);
             }
         }
         for (int w = tid; w < items; w += NT) {
             const int q = w / TPM;
             int rb, cb;
             split_item<MP>(w - q * TPM, RB, CB, rb, cb);
-            T *cout = PTR ? const_cast<T *>(ptab[(i % GS) * 3 * P + 2 * P + q])
+            T *cout = PTR ? const_cast<T *>(ptab[(i % gs) * 3 * P + 2 * P + q])
                           : p.C + (pair0 + q) * p.ldc2;
             if (DEVAB && b0r)
                 micro_tile<T, MS, NS, KS, OPA, OPB, true, MP>(sA + q * SA, sB + q * SB, nullptr,
@@ -1068,9 +1102,9 @@ __global__ void __launch_bounds__(NT) gather_kernel(const Params<T> p)
                                                          rb, cb, q, m, n, k, alpha, beta);
         }
         __syncthreads();
-        if constexpr (PTR) {  // slot i % GS is free: pointers of tile i + GS
-            store_regs(i + GS);
-            load_regs(i + GS + 1);
+        if constexpr (PTR) {  // slot i % gs is free: pointers of tile i + gs
+            store_regs(i + gs);
+            load_regs(i + gs + 1);
             __syncthreads();
         }
     }
