@@ -429,7 +429,8 @@ def e2e_of(wl, res, world, dev, args):
 
 
 # ------------------------------------------------------------ the gate
-def gate_sweep(dev, peak, batch=1_000_000, target_ms=12.0, max_reps=100):
+def gate_sweep(dev, peak, batch=1_000_000, target_ms=12.0, max_reps=100, kinds="sdcz",
+               sizes=range(1, 17), ops_filter=None):
     """Every type x n = 1..16 x every op pair x {beta == 0, general} at `batch` pairs:
     algorithmic GB/s as a fraction of the measured HBM peak.  Sustained protocol:
     rotating buffer sets whose total footprint is >= 4 x L2 (no set is L2-resident
@@ -441,14 +442,14 @@ def gate_sweep(dev, peak, batch=1_000_000, target_ms=12.0, max_reps=100):
     import txinputs
     from paper_1304_7053_b200 import model
 
-    pool_bytes = batch * 256 * 16  # one z16 operand at `batch` pairs
+    pool_bytes = batch * 256 * 16  # one z16 operand at `batch` pairs (larger n: fewer pairs)
     pools = [torch.empty(pool_bytes, dtype=torch.uint8, device=dev) for _ in range(3)]
     rdt = {"s": torch.float32, "d": torch.float64, "c": torch.float32, "z": torch.float64}
     cdt = {"s": torch.float32, "d": torch.float64, "c": torch.complex64, "z": torch.complex128}
     results = []
     cap_stream = torch.cuda.Stream()
     t0 = time.time()
-    for kind in "sdcz":
+    for kind in kinds:
         for j, pool in enumerate(pools):
             fill(pool.view(rdt[kind]), "d" if rdt[kind] == torch.float64 else "s",
                  txinputs.stream_key(txinputs.DEFAULT_SEED, "gate", kind, j), 0)
@@ -457,24 +458,27 @@ def gate_sweep(dev, peak, batch=1_000_000, target_ms=12.0, max_reps=100):
         betag = txinputs.scalar(kind, txinputs.stream_key(txinputs.DEFAULT_SEED, "gate", "b", kind))
         ops = "NTC" if kind in "cz" else "NT"
         es = model.ESIZE[kind]
-        for n in range(1, 17):
+        for n in sizes:
             e = n * n
-            per_op = batch * e * es
+            nb = min(batch, pool_bytes // (e * es))  # pairs per call (batch for n <= 16)
+            per_op = nb * e * es
             sets = max(1, min(pool_bytes // per_op, math.ceil(4 * L2_BYTES / (3 * per_op))))
             for ta in ops:
                 for tb in ops:
+                    if ops_filter and ta + tb not in ops_filter:
+                        continue
                     for beta0 in (True, False):
                         beta = 0 if beta0 else betag
-                        byts = model.bytes_moved(kind, n, n, n, batch, True, not beta0)
+                        byts = model.bytes_moved(kind, n, n, n, nb, True, not beta0)
                         reps = int(max(4, min(max_reps, target_ms / (byts / (peak * 1e6)))))
 
                         def call(r):
                             s = r % sets
-                            A = views[0][s * batch * e:(s + 1) * batch * e]
-                            B = views[1][s * batch * e:(s + 1) * batch * e]
-                            C = views[2][s * batch * e:(s + 1) * batch * e]
+                            A = views[0][s * nb * e:(s + 1) * nb * e]
+                            B = views[1][s * nb * e:(s + 1) * nb * e]
+                            C = views[2][s * nb * e:(s + 1) * nb * e]
                             rc = tx.tx_gemm_batched(kind, ta, tb, n, n, n, alpha, A, n, e, B, n, e,
-                                                    beta, C, n, e, batch)
+                                                    beta, C, n, e, nb)
                             assert rc == 0, tx.status_string(rc)
 
                         with torch.cuda.stream(cap_stream):
@@ -492,6 +496,7 @@ def gate_sweep(dev, peak, batch=1_000_000, target_ms=12.0, max_reps=100):
                         ms = a.elapsed_time(b) / reps
                         del g
                         results.append({"kind": kind, "n": n, "ops": ta + tb, "beta0": beta0,
+                                        "batch": nb, "path": tx.last_path()[0],
                                         "us": round(ms * 1e3, 3),
                                         "frac": round(byts / (ms / 1e3) / 1e9 / peak, 4),
                                         "sets": sets, "reps": reps})
