@@ -211,7 +211,8 @@ int tx_version(void);
 /* Path the calling thread's most recent successful GEMM call took:
  * 0 none/quick return, 1 packed bulk-copy (TMA) kernel, 2 general gather kernel,
  * 3 pointer-array kernel, 4 scale-only kernel (alpha == 0 or k == 0),
- * 5 register-direct kernel (packed square n <= 2);
+ * 5 register-direct kernel (packed square n <= 2),
+ * 6 tensor-core (tcgen05 split-TF32) kernel (packed s / c beyond 16);
  * +16 when a separate tail launch handled the last (< 16) pairs; +32 when the
  * kernel was a runtime-specialised (NVRTC, sm_100a) instance.  Also returns
  * the number of kernel launches of that call in *launches. */
@@ -229,6 +230,13 @@ int tx_set_tuning(int stages, int stage_kb);
  * TX_JIT=0 in the environment), 0 uses the generic-size AOT kernels.  Results are
  * bitwise identical either way.  Returns the previous setting. */
 int tx_set_jit(int enable);
+/* Tensor-core (tcgen05 split-TF32) kernel for packed s / c batches:
+ * -1 = automatic (default: the sizes where the FP32 FMA pipe bounds the CUDA-core
+ * kernels, or TX_TC=0/1 from the environment), 0 = never, 1 = wherever it applies
+ * (m, n, k <= 64 for s, <= 32 for c).  Results differ from the CUDA-core kernels
+ * only by rounding (same tolerance; bit-identical on integer-valued inputs).
+ * Process-wide; returns the previous setting (-1 when automatic). */
+int tx_set_tc(int mode);
 /* Number of instances JIT-compiled by this process (cache misses), or -1 when
  * NVRTC is unavailable. */
 int tx_jit_compiled(void);

@@ -23,7 +23,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("TXGEMM_LIB") or os.path.join(_HERE, "libtxgemm.so")
 
 KINDS = ("s", "d", "c", "z")
-PATHS = {0: "none", 1: "bulk", 2: "gather", 3: "ptr", 4: "scale", 5: "direct", 17: "bulk+tail",
+PATHS = {0: "none", 1: "bulk", 2: "gather", 3: "ptr", 4: "scale", 5: "direct", 6: "tc", 22: "tc+tail", 17: "bulk+tail",
          33: "bulk", 34: "gather", 35: "ptr", 49: "bulk+tail"}
 
 
@@ -96,6 +96,8 @@ def lib():
         L.tx_set_tuning.restype = ci
         L.tx_set_jit.argtypes = [ci]
         L.tx_set_jit.restype = ci
+        L.tx_set_tc.argtypes = [ci]
+        L.tx_set_tc.restype = ci
         L.tx_jit_compiled.restype = ci
         L.tx_prepare.argtypes = [cc, cc, cc, ci, ci, ci, ci, ci]
         L.tx_prepare.restype = ci
@@ -163,6 +165,12 @@ def last_path_jit() -> bool:
 
 def set_jit(enable: bool) -> int:
     return lib().tx_set_jit(1 if enable else 0)
+
+
+def set_tc(mode: int) -> int:
+    """Tensor-core split-TF32 kernel for packed s / c: -1 automatic, 0 never, 1 wherever
+    it applies.  Returns the previous setting."""
+    return lib().tx_set_tc(int(mode))
 
 
 def jit_compiled() -> int:

@@ -268,6 +268,38 @@ bool mma_jit_rule(bool cplx, int m, int n, int k, bool ptr)
     return cplx ? mx >= 13 : mx >= 17;
 }
 
+// tcgen05 split-TF32 kernel for s / c (TX_TC=0 never, =1 wherever it applies:
+// A/B measurements); unset: tc_rule, the sizes where the FP32 FMA pipe bounds the
+// CUDA-core kernels (tensor cores).
+static std::atomic<int> g_tc_override{-2};  // tx_set_tc; -2 = not set (environment)
+
+int tc_mode()
+{
+    const int o = g_tc_override.load();
+    if (o >= -1) return o;
+    static const int mode = [] {
+        const char *v = getenv("TX_TC");
+        if (!v || !*v) return -1;
+        return v[0] == '0' ? 0 : 1;
+    }();
+    return mode;
+}
+
+bool tc_rule(bool cplx, int m, int n, int k)
+{
+    const int mx = std::max(m, std::max(n, k));
+    return cplx ? mx >= 17 : mx >= 33;
+}
+
+// The kernel applies to packed s / c batches with m, n, k <= 64 (s) / 32 (c).
+static bool tc_applies(bool cplx, int m, int n, int k)
+{
+    const int lim = cplx ? 32 : 64;
+    if (m > lim || n > lim || k > lim) return false;
+    const int mode = tc_mode();
+    return mode == 1 || (mode < 0 && tc_rule(cplx, m, n, k));
+}
+
 // Register-direct kernel for n <= 2 (TX_DIRECT=0 disables it: A/B measurements).
 static bool direct_enabled()
 {
@@ -399,6 +431,17 @@ static int gemm_strided(char ta, char tb, int m, int n, int k, const U *alpha, c
             q.B += SB * c0;
             q.C += SC * c0;
             LaunchFn fn = nullptr;
+            if (tab.tc[opa][opb][b0] && tc_applies(AT::cplx, m, n, k)) {
+                Params<T> r = q;
+                r.P = unit;  // the alignment unit; the kernel's plan takes multiples of it
+                const cudaError_t e = tab.tc[opa][opb][b0](&r, st);
+                if (e == cudaSuccess) {
+                    path = PATH_TC;
+                    ++launches;
+                    continue;
+                }
+                if (e != cudaErrorNotSupported) return as_status(e);
+            }
             if (m == n && n == k && m <= 16) {
                 fn = tab.bulk_sq[opa][opb][b0][m - 1];
                 const int mode = mma_mode();
@@ -930,6 +973,13 @@ extern "C" int tx_set_tuning(int stages, int stage_kb)
 }
 
 extern "C" int tx_set_jit(int enable) { return jit_set_enabled(enable); }
+
+extern "C" int tx_set_tc(int mode)
+{
+    const int prev = tc_mode();
+    g_tc_override.store(mode < 0 ? -1 : (mode ? 1 : 0));
+    return prev;
+}
 
 extern "C" int tx_jit_compiled(void) { return jit_available() ? jit_compiled_count() : -1; }
 

@@ -20,7 +20,7 @@ enum { OP_N = 0, OP_T = 1, OP_C = 2 };
 
 // Path codes reported by tx_last_path() (include/txgemm.h).
 enum { PATH_NONE = 0, PATH_BULK = 1, PATH_GATHER = 2, PATH_PTR = 3, PATH_SCALE = 4,
-       PATH_DIRECT = 5, PATH_TAIL = 16, PATH_JIT = 32 };
+       PATH_DIRECT = 5, PATH_TC = 6, PATH_TAIL = 16, PATH_JIT = 32 };
 
 template <class T> struct is_cplx { static constexpr bool value = false; };
 template <> struct is_cplx<float2> { static constexpr bool value = true; };

@@ -2,6 +2,7 @@
 // m, n, k <= 16, gather kernels (general strided and pointer-array layouts),
 // and the alpha == 0 / k == 0 scale kernels.
 #include "tx_types.cuh"
+#include "tx_tc.cuh"
 
 namespace tx {
 namespace {
@@ -22,6 +23,11 @@ void fill_ops(TypeTables &t)
     t.direct[OPA][OPB][0][1] = &launch_direct<TxT, 2, OPA, OPB, false>;
     t.direct[OPA][OPB][1][1] = &launch_direct<TxT, 2, OPA, OPB, true>;
     t.count += 13;
+    if constexpr (TcOk<TxT>::value) {
+        t.tc[OPA][OPB][0] = &launch_tc<TxT, OPA, OPB, false>;
+        t.tc[OPA][OPB][1] = &launch_tc<TxT, OPA, OPB, true>;
+        t.count += 2;
+    }
 }
 }  // namespace
 
