@@ -479,7 +479,7 @@ def gate_sweep(dev, peak, batch=1_000_000, target_ms=12.0, max_reps=100, kinds="
                             C = views[2][s * nb * e:(s + 1) * nb * e]
                             rc = tx.tx_gemm_batched(kind, ta, tb, n, n, n, alpha, A, n, e, B, n, e,
                                                     beta, C, n, e, nb)
-                            assert rc == 0, tx.status_string(rc)
+                            assert rc == 0, f"{kind}{n} {ta}{tb} rc={rc}: {tx.status_string(rc)}"
 
                         with torch.cuda.stream(cap_stream):
                             call(0)  # warm: occupancy caches, attributes

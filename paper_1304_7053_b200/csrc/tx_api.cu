@@ -287,8 +287,15 @@ int tc_mode()
 
 bool tc_rule(bool cplx, int m, int n, int k)
 {
+    // From the interleaved A/B of the gate protocol (TX_TC=1 vs 0, squares 17-64 for s and
+    // 9-32 for c, N/N and T/T (c: N/N, C/T, T/C), both epilogues): the
+    // tensor-core kernel wins for s at 57 and above, and from 43 where a matrix's element
+    // count is not a multiple of 4 (the CUDA-core bulk path then needs 4-pair tiles and
+    // degrades), and for c from 29.
     const int mx = std::max(m, std::max(n, k));
-    return cplx ? mx >= 17 : mx >= 33;
+    if (cplx) return mx >= 29;
+    const bool odd = ((m * k) | (k * n) | (m * n)) & 3;
+    return mx >= 57 || (mx >= 43 && odd);
 }
 
 // The kernel applies to packed s / c batches with m, n, k <= 64 (s) / 32 (c).
@@ -368,6 +375,19 @@ static int gemm_strided(char ta, char tb, int m, int n, int k, const U *alpha, c
                         (one || (lda2 == SA && ldb2 == SB && ldc2 == SC)) && aligned16(A) &&
                         aligned16(B) && aligned16(C);
     int path = PATH_GATHER, launches = 0;
+    // tensor-core kernel (s / c beyond 16): packed leading dimensions, any element
+    // alignment (it copies 16-byte-aligned windows), the whole batch in one launch
+    const bool packed_ld = lda == rowsA && ldb == rowsB && ldc == m &&
+                           (one || (lda2 == SA && ldb2 == SB && ldc2 == SC));
+    if (packed_ld && tab.tc[opa][opb][b0] && tc_applies(AT::cplx, m, n, k)) {
+        const cudaError_t e = tab.tc[opa][opb][b0](&p, st);
+        if (e == cudaSuccess) {
+            t_last_path = PATH_TC;
+            t_last_launches = 1;
+            return 0;
+        }
+        if (e != cudaErrorNotSupported) return as_status(e);
+    }
     // fixed-operand batches (the paper's §9 variant): A and/or B shared by every pair
     const bool bcA = !one && lda2 == 0 && lda == rowsA;
     const bool bcB = !one && ldb2 == 0 && ldb == rowsB;
@@ -431,17 +451,6 @@ static int gemm_strided(char ta, char tb, int m, int n, int k, const U *alpha, c
             q.B += SB * c0;
             q.C += SC * c0;
             LaunchFn fn = nullptr;
-            if (tab.tc[opa][opb][b0] && tc_applies(AT::cplx, m, n, k)) {
-                Params<T> r = q;
-                r.P = unit;  // the alignment unit; the kernel's plan takes multiples of it
-                const cudaError_t e = tab.tc[opa][opb][b0](&r, st);
-                if (e == cudaSuccess) {
-                    path = PATH_TC;
-                    ++launches;
-                    continue;
-                }
-                if (e != cudaErrorNotSupported) return as_status(e);
-            }
             if (m == n && n == k && m <= 16) {
                 fn = tab.bulk_sq[opa][opb][b0][m - 1];
                 const int mode = mma_mode();
@@ -459,6 +468,16 @@ static int gemm_strided(char ta, char tb, int m, int n, int k, const U *alpha, c
             // (an AOT tensor-copy instance whose tensor map cannot be encoded also
             // reports cudaErrorNotSupported: the generic bulk kernel takes over)
             if (e == cudaErrorNotSupported) e = tab.bulk_dyn[opa][opb][b0](&q, st);
+            // two stages of one alignment unit of pairs exceed shared memory (odd sizes
+            // beyond ~48): the gather kernels, which need no alignment unit
+            if (e == cudaErrorNotSupported) {
+                e = launch_jit<T>(JIT_GATHER, q, opa, opb, b0, st);
+                if (e == cudaSuccess) path = PATH_GATHER | PATH_JIT;
+                if (e == cudaErrorNotSupported) {
+                    e = tab.gather[opa][opb][b0][0](&q, st);
+                    path = PATH_GATHER;
+                }
+            }
             if (e != cudaSuccess) return as_status(e);
             ++launches;
         }
@@ -557,6 +576,10 @@ static int gemm_strided_dev(char ta, char tb, int m, int n, int k, const U *alph
             e = launch_jit<T>(JIT_BULK, q, opa, opb, false, st, 0, true);
             path = PATH_BULK | (e == cudaSuccess ? PATH_JIT : 0);
             if (e == cudaErrorNotSupported) e = tab.bulk_dyn_dev[opa][opb](&q, st);
+            if (e == cudaErrorNotSupported) {  // does not fit (see gemm_strided): gather
+                e = tab.gather_dev[opa][opb][0](&q, st);
+                path = PATH_GATHER;
+            }
             if (e != cudaSuccess) return as_status(e);
             ++launches;
         }

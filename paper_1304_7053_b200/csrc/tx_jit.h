@@ -143,6 +143,7 @@ cudaError_t launch_jit(JitKind kind, Params<T> p, int opa, int opb, bool b0, cud
         pl.smem = pl.S * 128 * (SA + SB + (b0 ? 0 : SC)) * (int)sizeof(T) + 8 * pl.S;
     }
     if (kind == JIT_BULK_PTR) pl.smem += pl.S * pl.P * 8;  // the C-pointer slots
+    if (pl.smem > SMEM_MAX_BYTES) return cudaErrorNotSupported;  // the caller gathers
     p.P = pl.P;
     p.S = pl.S;
     p.ntiles = pl.ntiles;

@@ -925,7 +925,13 @@ __global__ void __launch_bounds__(NT) gather_kernel(const Params<T> p)
     const int rowsB = (OPB == OP_N) ? k : n;
     const int P = p.P;
     const int gs = p.S;  // ring depth (3, or 2 when three stages of the tile do not fit)
-    const int stage_elems = P * (SA + SB + (B0 ? 0 : SC));
+    // operand regions of a stage start on 16-byte boundaries, so P needs no alignment
+    // unit (a matrix whose elements are vector-read has a size that is a multiple of
+    // the vector width; host: plan_tiles with bulk = false)
+    constexpr int E16 = 16 / (int)sizeof(T) > 0 ? 16 / (int)sizeof(T) : 1;  // elements per 16 B
+    const int oB = (P * SA + E16 - 1) / E16 * E16;
+    const int oC = oB + (P * SB + E16 - 1) / E16 * E16;
+    const int stage_elems = oC + (B0 ? 0 : (P * SC + E16 - 1) / E16 * E16);
     T *stage0 = reinterpret_cast<T *>(smem_raw);
     const T **ptab = reinterpret_cast<const T **>(
         smem_raw + (((long long)gs * stage_elems * sizeof(T) + 15) & ~15ll));
@@ -1011,12 +1017,12 @@ __global__ void __launch_bounds__(NT) gather_kernel(const Params<T> p)
         T *st = stage0 + (long long)(i % gs) * stage_elems;
         if constexpr (V16) {
             chunks16(i, 0, st, SA, np, pair0, p.A, p.lda2);
-            chunks16(i, 1, st + P * SA, SB, np, pair0, p.B, p.ldb2);
-            if (!b0r) chunks16(i, 2, st + P * (SA + SB), SC, np, pair0, p.C, p.ldc2);
+            chunks16(i, 1, st + oB, SB, np, pair0, p.B, p.ldb2);
+            if (!b0r) chunks16(i, 2, st + oC, SC, np, pair0, p.C, p.ldc2);
         } else {
             elems(i, 0, st, SA, rowsA, p.lda, np, pair0, p.A, p.lda2);
-            elems(i, 1, st + P * SA, SB, rowsB, p.ldb, np, pair0, p.B, p.ldb2);
-            if (!b0r) elems(i, 2, st + P * (SA + SB), SC, m, p.ldc, np, pair0, p.C, p.ldc2);
+            elems(i, 1, st + oB, SB, rowsB, p.ldb, np, pair0, p.B, p.ldb2);
+            if (!b0r) elems(i, 2, st + oC, SC, m, p.ldc, np, pair0, p.C, p.ldc2);
         }
     };
 
@@ -1064,7 +1070,7 @@ __global__ void __launch_bounds__(NT) gather_kernel(const Params<T> p)
         const long long pair0 = (blockIdx.x + (long long)i * G) * P;
         const int np = (int)min((long long)P, p.batch - pair0);
         const T *st = stage0 + (long long)(i % gs) * stage_elems;
-        const T *sA = st, *sB = st + P * SA, *sC = st + P * (SA + SB);
+        const T *sA = st, *sB = st + oB, *sC = st + oC;
         const int items = MMA ? 0 : np * TPM;
         if constexpr (MMA) {  // FP64 tensor cores: one warp per macro-tile
             const int warp = tid >> 5, lane = tid & 31;

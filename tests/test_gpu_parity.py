@@ -569,6 +569,45 @@ def test_sizes_beyond_16(kind, mnk):
     check(kind, "T", "T", m, n, k, alpha, beta, A, B, C, got, ref)
 
 
+@pytest.mark.parametrize("kind,mnk", [("s", (51, 51, 51)), ("s", (63, 63, 63)), ("s", (57, 49, 61)),
+                                      ("d", (63, 63, 63)), ("d", (49, 51, 53)), ("d", (37, 41, 43))],
+                         ids=lambda v: v if isinstance(v, str) else "x".join(map(str, v)))
+def test_odd_large_sizes_every_path(kind, mnk):
+    """Odd sizes near the limit: two ring stages of one 16-byte alignment unit of pairs
+    (4 pairs for s, 2 for d) exceed shared memory, so the packed CUDA-core path hands the
+    batch to the gather kernels, whose stage regions are 16-byte aligned for any tile size
+    (round 2 fix: these calls returned 'invalid argument').  Packed with the tensor-core
+    kernel disabled, padded, and pointer arrays, each against the oracle."""
+    import torch
+    from paper_1304_7053_b200 import binding
+
+    m, n, k = mnk
+    prev = binding.set_tc(0)
+    try:
+        for ta, tb in (("N", "N"), ("T", "T")):
+            for general in (False, True):
+                _case(kind, m, n, k, 37, ta, tb, general, "oddbig")
+                _case(kind, m, n, k, 29, ta, tb, general, "oddbigpad", pad=(1, 5))
+        A, B, C = random_case(kind, m, n, k, 31, "N", "T", seed=12, tag="oddptr")
+        alpha, beta = _ab(kind, "oddptr")
+        dA, _ = to_dev(A)
+        dB, _ = to_dev(B)
+        dC, _ = to_dev(C)
+        es = dA.element_size()
+        perm = np.random.default_rng(3).permutation(C.batch)
+        pa = torch.tensor(A.offsets()[perm] * es + dA.data_ptr(), device="cuda")
+        pb = torch.tensor(B.offsets()[perm] * es + dB.data_ptr(), device="cuda")
+        pc = torch.tensor(C.offsets()[perm] * es + dC.data_ptr(), device="cuda")
+        rc = tx.tx_gemm_batched_ptr(kind, "N", "T", m, n, k, alpha, pa, A.ld, pb, B.ld, beta, pc,
+                                    C.ld, C.batch)
+        assert rc == 0, tx.status_string(rc)
+        got = dC.cpu().numpy()
+        ref = run_oracle(kind, "N", "T", m, n, k, alpha, beta, A, B, C)
+        check(kind, "N", "T", m, n, k, alpha, beta, A, B, C, got, ref)
+    finally:
+        binding.set_tc(prev)
+
+
 @pytest.mark.parametrize("kind", "sdcz")
 @pytest.mark.parametrize("mnk", [(32, 32, 32), (24, 8, 32), (5, 30, 32), (64, 64, 64), (48, 40, 16)],
                          ids=lambda t: "x".join(map(str, t)))

@@ -122,7 +122,7 @@ def test_tc_beta0_never_reads_C(kind):
     check(kind, "N", "N", m, n, k, alpha, 0, A, B, C, got, ref)
 
 
-@pytest.mark.parametrize("kind,n", [("s", 64), ("s", 40), ("c", 32), ("c", 24)])
+@pytest.mark.parametrize("kind,n", [("s", 64), ("s", 45), ("c", 32), ("c", 29)])
 def test_tc_default_rule_and_batch_edges(kind, n):
     """The automatic rule picks the tensor-core kernel at these sizes; batches 1, 2, 3,
     149 (one pair per SM and a few over), and a large odd batch."""
@@ -133,3 +133,22 @@ def test_tc_default_rule_and_batch_edges(kind, n):
         assert rc == 0 and path[0] in ("tc", "tc+tail"), path
         ref = run_oracle(kind, "N", "N", n, n, n, alpha, beta, A, B, C)
         check(kind, "N", "N", n, n, n, alpha, beta, A, B, C, got, ref)
+
+
+@pytest.mark.parametrize("kind,mnk", [("s", (51, 51, 51)), ("s", (63, 61, 59)), ("c", (31, 29, 27)),
+                                      ("c", (17, 19, 23))],
+                         ids=lambda v: v if isinstance(v, str) else "x".join(map(str, v)))
+@pytest.mark.parametrize("misalign", [0, 1, 3])
+def test_tc_any_element_alignment(kind, mnk, misalign):
+    """Packed batches whose per-pair byte sizes are not multiples of 16 and whose bases are
+    only element-aligned: the kernel copies the 16-byte-aligned windows covering each
+    tile, so every pair -- and the whole batch, no tail launch -- runs on it."""
+    m, n, k = mnk
+    with tc_forced():
+        for general in (False, True):
+            A, B, C = random_case(kind, m, n, k, 157, "N", "T", seed=41, tag="tcwin")
+            alpha, beta = _ab(kind, f"win{m}{misalign}", general)
+            rc, got, path = run_lib(kind, "N", "T", m, n, k, alpha, beta, A, B, C, misalign=misalign)
+            assert rc == 0 and path == ("tc", 1), path
+            ref = run_oracle(kind, "N", "T", m, n, k, alpha, beta, A, B, C)
+            check(kind, "N", "T", m, n, k, alpha, beta, A, B, C, got, ref)

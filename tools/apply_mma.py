@@ -26,12 +26,24 @@ def key_of(r):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--autotune", nargs="+", required=True)
+    ap.add_argument("--autotune", nargs="*", default=[],
+                    help="autotune lines; without them S, KB are kept from the current table")
     ap.add_argument("--ab-on", nargs="*", default=[])
     ap.add_argument("--ab-off", nargs="*", default=[])
     ap.add_argument("--margin", type=float, default=1.02)
     a = ap.parse_args()
     tune = defaultdict(lambda: defaultdict(list))
+    if not a.autotune:  # keep the table's (S, KB); only the ON column is re-decided
+        import re
+        rx = re.compile(r"TX_MMAMAP\((\w+), (\d+), (\d), (\d), (\d), (\d+), (\d+), \d\)")
+        name = {v: k for k, v in KIND.items()}
+        opn = {v: k for k, v in OPC.items()}
+        for line in open(TABLE):
+            mt = rx.search(line)
+            if mt:
+                t, n, oa, ob, b0, S, KB = mt.groups()
+                key = (name[t], int(n), opn[int(oa)] + opn[int(ob)], b0 == "1")
+                tune[key][(int(S), int(KB))].append(1.0)
     for path in a.autotune:
         for line in open(path):
             r = json.loads(line)
@@ -43,7 +55,7 @@ def main():
         for path in paths:
             for line in open(path):
                 r = json.loads(line)
-                acc[key_of(r)].append(r["frac_measured"])
+                acc[key_of(r)].append(r.get("frac_measured", r.get("frac")))
         return {k: statistics.mean(v) for k, v in acc.items()}
 
     on, off = avg(a.ab_on), avg(a.ab_off)

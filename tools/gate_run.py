@@ -41,9 +41,17 @@ def main():
 
     torch.cuda.set_device(0)
     peak, _ = bench.peaks()
-    res, wall = bench.gate_sweep("cuda:0", peak, batch=a.batch, kinds=a.kinds,
-                                 sizes=sizes_of(a.sizes),
-                                 ops_filter=set(a.ops.split(",")) if a.ops else None)
+    res, wall = [], 0.0
+    for kind in a.kinds:
+        for n in sizes_of(a.sizes):
+            try:
+                r, w = bench.gate_sweep("cuda:0", peak, batch=a.batch, kinds=kind, sizes=[n],
+                                        ops_filter=set(a.ops.split(",")) if a.ops else None)
+                res += r
+                wall += w
+            except AssertionError as e:  # a failing call: record it, go on
+                res.append({"kind": kind, "n": n, "error": str(e)})
+                print(f"{kind}{n}: {e}", file=sys.stderr)
     with open(a.out, "w") as f:
         for r in res:
             r["tag"] = a.tag

@@ -4,6 +4,8 @@
 // shared memory in the 128-byte-swizzled canonical layout, one thread issues
 // tcgen05.mma.cta_group::1.kind::tf32 (M = 128) over K in steps of 8, the four warps
 // read the accumulator back with tcgen05.ld.32x32b and write D (128 x N, row-major).
+// M = 64 or 128 (the M = 64 run reports where D's rows land in TMEM: row r of D in
+// lane L of the output when D[L][*] holds row r's values).
 // nsets = 1: D = A0 B0^T; nsets = 3: D = A0 B1^T + A1 B0^T + A0 B0^T (the 3xTF32 order
 // with A0/B0 = hi, A1/B1 = lo parts), all into one accumulator.
 //
@@ -46,7 +48,7 @@ __device__ __forceinline__ uint32_t idesc_tf32(int M, int N, int nega, int negb)
 
 __global__ void __launch_bounds__(128, 1)
 probe_kernel(const float *A0, const float *A1, const float *B0, const float *B1, float *D, int N,
-             int K, int nsets)
+             int K, int nsets, int M)
 {
     extern __shared__ __align__(1024) unsigned char smem[];
     __shared__ uint32_t tmem_base;
@@ -83,7 +85,7 @@ probe_kernel(const float *A0, const float *A1, const float *B0, const float *B1,
     asm volatile("tcgen05.fence::after_thread_sync;");
     const uint32_t tmem = tmem_base;
     if (tid == 0) {
-        const uint32_t id = idesc_tf32(128, N, 0, 0);
+        const uint32_t id = idesc_tf32(M, N, 0, 0);
         int first = 1;
         for (int s = 0; s < K / 8; ++s) {
             const uint32_t kb = s >> 2, kin = (s & 3) * 32;
@@ -127,12 +129,12 @@ probe_kernel(const float *A0, const float *A1, const float *B0, const float *B1,
 }  // namespace
 
 extern "C" int tc_probe(const float *A0, const float *A1, const float *B0, const float *B1, float *D,
-                        int N, int K, int nsets)
+                        int N, int K, int nsets, int M)
 {
     const int KB = (K + 31) / 32;
     const size_t smem = (size_t)KB * 128 * (2 * 128 + 2 * N) + 1024;
     cudaFuncSetAttribute(probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    probe_kernel<<<1, 128, smem>>>(A0, A1, B0, B1, D, N, K, nsets);
+    probe_kernel<<<1, 128, smem>>>(A0, A1, B0, B1, D, N, K, nsets, M);
     cudaError_t e = cudaDeviceSynchronize();
     return (int)e;
 }

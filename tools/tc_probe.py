@@ -43,13 +43,13 @@ def main():
     L = ctypes.CDLL(SO)
     rng = np.random.default_rng(7)
 
-    def run(A0, B0, N, K, A1=None, B1=None, nsets=1):
+    def run(A0, B0, N, K, A1=None, B1=None, nsets=1, M=128):
         A1 = np.zeros_like(A0) if A1 is None else A1
         B1 = np.zeros_like(B0) if B1 is None else B1
         t = [torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32)).cuda() for x in (A0, A1, B0, B1)]
         D = torch.zeros(128, N, dtype=torch.float32, device="cuda")
         rc = L.tc_probe(*(ctypes.c_void_p(x.data_ptr()) for x in t), ctypes.c_void_p(D.data_ptr()),
-                        N, K, nsets)
+                        N, K, nsets, M)
         assert rc == 0, rc
         return D.cpu().numpy()
 
@@ -100,6 +100,28 @@ def main():
         res.append({"K": K, "max_err_3xtf32": float(np.max(np.abs(D3 - ref) / den)),
                     "max_err_1xtf32": float(np.max(np.abs(D1 - ref) / den))})
     out["split3"] = res
+
+    # M = 64: A row i = (i + 1, 0, ...), B = e_0 -> D[i][j] = i + 1 for i < 64; where is row i?
+    A = np.zeros((128, 32), np.float32)
+    A[:64, 0] = np.arange(1, 65)
+    A[64:, 0] = 1000 + np.arange(64)  # rows the M = 64 MMA must not read
+    B = np.zeros((16, 32), np.float32)
+    B[:, 0] = 1
+    D = run(A, B, 16, 32, M=64)
+    lanes = {}
+    for ln in range(128):
+        v = D[ln, 0]
+        lanes[ln] = int(v) - 1 if 0 < v <= 64 and np.all(D[ln] == v) else None
+    out["m64_row_of_lane"] = lanes
+    rows = {r: [ln for ln, rr in lanes.items() if rr == r] for r in range(64)}
+    out["m64_lane_of_row_rule_16x4"] = all(rows[r] == [32 * (r // 16) + r % 16] for r in range(64))
+    # layout check at M = 64 with integers
+    A = rng.integers(-8, 9, (128, 64)).astype(np.float32)
+    B = rng.integers(-8, 9, (40, 64)).astype(np.float32)
+    D = run(A, B, 40, 64, M=64)
+    ref = A[:64].astype(np.float64) @ B.astype(np.float64).T
+    got = np.stack([D[32 * (r // 16) + r % 16] for r in range(64)])
+    out["m64_exact_16x4_rule"] = bool(np.array_equal(got, ref))
     print(json.dumps(out, indent=1))
 
 
