@@ -317,6 +317,17 @@ static bool direct_enabled()
     return on;
 }
 
+// Smallest matrix (bytes) for which a packed pointer-array batch takes the per-matrix
+// bulk-copy kernel instead of the 16-byte gather (TX_PTR_BULK_MIN: A/B measurements).
+static int ptr_bulk_min_bytes()
+{
+    static const int v = [] {
+        const char *e = getenv("TX_PTR_BULK_MIN");
+        return e && *e ? atoi(e) : 512;
+    }();
+    return v;
+}
+
 // Pairs per bulk launch (a multiple of every 16-byte alignment unit): keeps the
 // 32-bit TMA row coordinates pair * rows (rows <= 32) below 2^31.
 constexpr long long BULK_CHUNK_PAIRS = 1ll << 26;
@@ -705,7 +716,8 @@ static int gemm_ptr(char ta, char tb, int m, int n, int k, const U *alpha, const
         // small matrices: 16-byte cp.async chunks over all threads (a per-matrix
         // TMA copy costs ~80 cycles of issue); >= 512-byte matrices: TMA per matrix
         const int min_bytes = es * std::min(m * k, std::min(k * n, m * n));
-        const JitKind kind = !bulk_ok ? JIT_GATHER_PTR : (min_bytes >= 512 ? JIT_BULK_PTR : JIT_GATHER_PTR16);
+        const JitKind kind = !bulk_ok ? JIT_GATHER_PTR
+                                      : (min_bytes >= ptr_bulk_min_bytes() ? JIT_BULK_PTR : JIT_GATHER_PTR16);
         e = launch_jit<T>(kind, p, opa, opb, b0, st);
         t_last_path = PATH_PTR | (e == cudaSuccess ? PATH_JIT : 0);
         if (e == cudaErrorNotSupported) e = tab.gather[opa][opb][b0][1](&p, st);
