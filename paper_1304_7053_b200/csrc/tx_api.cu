@@ -263,7 +263,9 @@ int mma_mode()
 // tensor-core instance where measured faster (DMMA).
 bool mma_jit_rule(bool cplx, int m, int n, int k, bool ptr)
 {
-    (void)ptr;
+    // pointer arrays with m or n below one 8 x 8 fragment: mostly padding (ptr A/B, round 2:
+    // z 1x16x16 0.69 -> 0.91 of HBM and z 16x3x16 0.56 -> 0.92 without, profiles/r02s3_ptr_ab)
+    if (ptr && std::min(m, n) < 8) return false;
     const int mx = std::max(m, std::max(n, k));
     return cplx ? mx >= 13 : mx >= 17;
 }

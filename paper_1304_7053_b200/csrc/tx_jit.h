@@ -80,7 +80,11 @@ cudaError_t launch_jit(JitKind kind, Params<T> p, int opa, int opb, bool b0, cud
         expr += mp.BSW ? ", true" : ", false";
         if (mma) expr += ", true";
     }
-    if (kind == JIT_BULK_PTR && mma) expr += ", true";
+    // bulk_ptr_kernel<..., MMA, DEC>: the decoupled ring for 8- and 16-byte types with a
+    // C input (pointer-array A/B, round 2, profiles/r02s3_ptr_ab_dec.jsonl: d16 general
+    // 0.58 -> 0.85 of HBM; it lost on beta = 0 and on s: c16 beta = 0 0.72 -> 0.57)
+    const bool dec = kind == JIT_BULK_PTR && !b0 && sizeof(T) >= 8;
+    if (kind == JIT_BULK_PTR) expr += std::string(mma ? ", true" : ", false") + (dec ? ", true" : ", false");
     const bool swz = kind == JIT_BULK && (mp.ASW || mp.BSW);
     if (kind == JIT_BULK && (bcast || devab || swz || mma)) {  // <..., BCAST, TRA, DEVAB, ASW, BSW[, MMA]>
         expr += ", " + std::to_string(bcast) + ", false";
@@ -97,13 +101,15 @@ cudaError_t launch_jit(JitKind kind, Params<T> p, int opa, int opb, bool b0, cud
         const char *v = getenv("TX_GATHER_KB");
         return v ? atoi(v) : 0;
     }();
-    const int kb = gather && gather_kb > 0 ? gather_kb : mp.KB;
+    // bulk_ptr: two stages of ~16 KB (pointer-array A/B over S x KB, round 2: s16 general
+    // 0.54 -> 0.95, z16 beta = 0 0.38 -> 0.85 of HBM against the strided instance's plan)
+    const int kb = gather && gather_kb > 0 ? gather_kb : (kind == JIT_BULK_PTR ? 16 : mp.KB);
     static const bool two_ctas = [] {  // TX_PLAN_2CTA=0: the plain planner (A/B runs)
         const char *v = getenv("TX_PLAN_2CTA");
         return !(v && v[0] == '0');
     }();
     Plan pl = plan_tiles(sizeof(T), p.m, p.n, p.k, b0, mp.RM, mp.RN, NT, p.batch, !gather,
-                         gather ? GS : mp.S, kb, kind == JIT_BULK ? bcast : 0, 0, rows_cap,
+                         gather ? GS : (kind == JIT_BULK_PTR ? 2 : mp.S), kb, kind == JIT_BULK ? bcast : 0, 0, rows_cap,
                          kind == JIT_BULK && two_ctas, mma ? 32 * mma_items(cplx, p.m, p.n) : 0);
     if (swz) {
         // the 1024-byte alignment of the swizzled regions: shrink the tile until it fits
@@ -140,7 +146,7 @@ cudaError_t launch_jit(JitKind kind, Params<T> p, int opa, int opb, bool b0, cud
         pl.P = 128;
         pl.ntiles = (int)(((long long)p.batch + 127) / 128);
         const int SA = p.m * p.k, SB = p.k * p.n, SC = p.m * p.n;
-        pl.smem = pl.S * 128 * (SA + SB + (b0 ? 0 : SC)) * (int)sizeof(T) + 8 * pl.S;
+        pl.smem = pl.S * 128 * (SA + SB + (b0 ? 0 : SC)) * (int)sizeof(T) + 16 * pl.S;  // full + empty barriers
     }
     if (kind == JIT_BULK_PTR) pl.smem += pl.S * pl.P * 8;  // the C-pointer slots
     if (pl.smem > SMEM_MAX_BYTES) return cudaErrorNotSupported;  // the caller gathers

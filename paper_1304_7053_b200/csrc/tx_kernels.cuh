@@ -594,13 +594,34 @@ __global__ void __launch_bounds__(NT) bulk_kernel(const __grid_constant__ Params
         (((long long)S * stage_elems + (BA ? SA : 0) + (BB ? SB : 0) + tr_elems) * sizeof(T) + 15) /
             16 * 16);
 
+    // Decoupled ring (build with -DTX_DEC; all but TRA, whose transposed copy is a
+    // CTA-wide buffer): bars[s] = "stage s full" (the copies' bytes), empty[s] = "stage s
+    // consumed" (one arrive per warp).  Thread 0 refills a stage once every warp has
+    // released it, so no warp waits at a CTA barrier for the slowest one; the warps'
+    // item assignment rotates by one warp per tile so a tile's partial last pass over
+    // the thread block lands on each warp in turn.  Motivated by ncu (c13 beta = 0: 1.9
+    // of 5.9 cycles per issued instruction were barrier stalls at the per-tile
+    // __syncthreads), but an interleaved gate A/B over all 832 square instances measured
+    // no net gain (median ratio 0.999, 104 instances faster and 173 slower by > 2 %,
+    // c13 beta = 0 0.94x; profiles/r02s3_dec_ab/), so the default build keeps the
+    // per-tile __syncthreads ring.
+#ifdef TX_DEC
+    constexpr bool DEC = !TRA;
+#else
+    constexpr bool DEC = false;
+#endif
+    constexpr int NW = NT / 32;
+    uint64_t *empty = bars + S;
     const int tid = threadIdx.x;
     const int G = gridDim.x;
     const int my_tiles = (p.ntiles - (int)blockIdx.x + G - 1) / G;
     const uint64_t pol = policy_evict_first();
 
     if (tid == 0) {
-        for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
+        for (int s = 0; s < S; ++s) {
+            mbar_init(&bars[s], 1);
+            if (DEC) mbar_init(&empty[s], NW);
+        }
         fence_mbar_init();
     }
     __syncthreads();
@@ -670,7 +691,14 @@ __global__ void __launch_bounds__(NT) bulk_kernel(const __grid_constant__ Params
         for (int i = 0; i < S - 1 && i < my_tiles; ++i) issue(i);
 
     for (int i = 0; i < my_tiles; ++i) {
-        if (tid == 0 && i + S - 1 < my_tiles) issue(i + S - 1);
+        if (tid == 0 && i + S - 1 < my_tiles) {
+            // tile i + S - 1 reuses the stage of tile i - 1
+            if (DEC && i >= 1) mbar_wait(&empty[(i - 1) % S], ((i - 1) / S) & 1);
+            issue(i + S - 1);
+        }
+        // rotated thread / warp index of this tile (DEC)
+        const int rw = DEC ? ((tid >> 5) + i) % NW : (tid >> 5);
+        const int rt = DEC ? rw * 32 + (tid & 31) : tid;
         const long long pair0 = (blockIdx.x + (long long)i * G) * P;
         const int np = (int)min((long long)P, p.batch - pair0);
         const T *st = stage0 + (long long)(i % S) * stage_elems;
@@ -698,16 +726,16 @@ __global__ void __launch_bounds__(NT) bulk_kernel(const __grid_constant__ Params
                     gC + q * SC, m, rb, cb, q, m, n, k, p.alpha, p.beta);
             }
         } else if constexpr (MMA) {
-            const int warp = tid >> 5, lane = tid & 31;
+            const int lane = tid & 31;
             constexpr int IT = MmaShape<T, (MS > 0 ? MS : 1), (NS > 0 ? NS : 1)>::ITEMS;
-            for (int w = warp; w < np * IT; w += NT / 32) {
+            for (int w = rw; w < np * IT; w += NT / 32) {
                 const int q = w / IT;
                 mma_item<T, MS, NS, KS, OPA, OPB, B0>(sA + q * SA, sB + q * SB,
                                                       B0 ? nullptr : sC + q * SC, gC + q * SC, m,
                                                       w - q * IT, lane, alpha, beta);
             }
         } else if (DEVAB && b0r) {  // run-time beta == 0: C is never read
-            for (int w = tid; w < items; w += NT) {
+            for (int w = rt; w < items; w += NT) {
                 const int q = w / TPM;
                 int rb, cb;
                 split_item<MP>(w - q * TPM, RB, CB, rb, cb);
@@ -716,7 +744,7 @@ __global__ void __launch_bounds__(NT) bulk_kernel(const __grid_constant__ Params
                                                               alpha, beta);
             }
         } else if constexpr (SWZ) {
-            for (int w = tid; w < items; w += NT) {
+            for (int w = rt; w < items; w += NT) {
                 const int q = w / TPM;
                 int rb, cb;
                 split_item<MP>(w - q * TPM, RB, CB, rb, cb);
@@ -729,7 +757,7 @@ __global__ void __launch_bounds__(NT) bulk_kernel(const __grid_constant__ Params
                     a_rs, q * m, b_rs, q * n);
             }
         } else {
-            for (int w = tid; w < items; w += NT) {
+            for (int w = rt; w < items; w += NT) {
                 const int q = w / TPM;
                 int rb, cb;
                 split_item<MP>(w - q * TPM, RB, CB, rb, cb);
@@ -740,7 +768,12 @@ __global__ void __launch_bounds__(NT) bulk_kernel(const __grid_constant__ Params
                                                             alpha, beta);
             }
         }
-        __syncthreads();  // stage i % S fully consumed before it is refilled
+        if constexpr (DEC) {  // this warp is done with stage i % S
+            __syncwarp();
+            if ((tid & 31) == 0) mbar_arrive(&empty[i % S]);
+        } else {
+            __syncthreads();  // stage i % S (and the transposed copy) fully consumed
+        }
     }
 }
 
@@ -754,8 +787,10 @@ __global__ void __launch_bounds__(NT) bulk_kernel(const __grid_constant__ Params
 // mbarrier (its bytes are excluded from the expected count).
 // P <= 32 * PPL pairs per tile.
 // --------------------------------------------------------------------------
+// DEC: the decoupled ring of bulk_kernel (empty mbarriers, rotated warp items) instead of
+// the per-tile __syncthreads; chosen per call by the host (pointer-array A/B, round 2).
 template <class T, int MS, int NS, int KS, int OPA, int OPB, bool B0, class MP, int NT,
-          bool MMA = false>
+          bool MMA = false, bool DEC = false>
 __global__ void __launch_bounds__(NT) bulk_ptr_kernel(const Params<T> p)
 {
     constexpr int PPL = 4;  // pointer triples per lane (P <= 128)
@@ -770,13 +805,18 @@ __global__ void __launch_bounds__(NT) bulk_ptr_kernel(const Params<T> p)
     uint64_t *bars = reinterpret_cast<uint64_t *>(stage0 + (long long)S * stage_elems);
     // the tile's C pointers, one slot per stage: written by warp 0 with the copies,
     // read by every thread's epilogue (no dependent global load in the compute loop)
-    T **cptr = reinterpret_cast<T **>(bars + S);
+    // decoupled ring as in bulk_kernel: empty[s] = "stage s consumed" (one arrive per warp)
+    uint64_t *empty = bars + S;
+    T **cptr = reinterpret_cast<T **>(bars + 2 * S);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int G = gridDim.x;
     const int my_tiles = (p.ntiles - (int)blockIdx.x + G - 1) / G;
     const uint64_t pol = policy_evict_first();
     if (tid == 0) {
-        for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
+        for (int s = 0; s < S; ++s) {
+            mbar_init(&bars[s], 1);
+            if (DEC) mbar_init(&empty[s], NT / 32);
+        }
         fence_mbar_init();
     }
     __syncthreads();
@@ -854,6 +894,8 @@ __global__ void __launch_bounds__(NT) bulk_ptr_kernel(const Params<T> p)
     }
     for (int i = 0; i < my_tiles; ++i) {
         if (warp == 0 && i + S - 1 < my_tiles) {
+            // tile i + S - 1 reuses the stage (and C-pointer slots) of tile i - 1
+            if (DEC && i >= 1) mbar_wait(&empty[(i - 1) % S], ((i - 1) / S) & 1);
             issue(i + S - 1);
             load_ptrs(i + S);  // consumed next iteration; latency overlaps this tile's compute
         }
@@ -861,10 +903,12 @@ __global__ void __launch_bounds__(NT) bulk_ptr_kernel(const Params<T> p)
         const int np = (int)min((long long)P, p.batch - pair0);
         const T *st = stage0 + (long long)(i % S) * stage_elems;
         const T *sA = st, *sB = st + P * SA, *sC = st + P * (SA + SB);
+        const int rw = DEC ? (warp + i) % (NT / 32) : warp;  // rotated warp / thread index
+        const int rt = rw * 32 + lane;
         mbar_wait(&bars[i % S], (i / S) & 1);
         if constexpr (MMA) {  // FP64 tensor cores: one warp per macro-tile
             constexpr int IT = MmaShape<T, (MS > 0 ? MS : 1), (NS > 0 ? NS : 1)>::ITEMS;
-            for (int w = warp; w < np * IT; w += NT / 32) {
+            for (int w = rw; w < np * IT; w += NT / 32) {
                 const int q = w / IT;
                 mma_item<T, MS, NS, KS, OPA, OPB, B0>(sA + q * SA, sB + q * SB,
                                                       B0 ? nullptr : sC + q * SC,
@@ -873,7 +917,7 @@ __global__ void __launch_bounds__(NT) bulk_ptr_kernel(const Params<T> p)
             }
         } else {
             const int items = np * TPM;
-            for (int w = tid; w < items; w += NT) {
+            for (int w = rt; w < items; w += NT) {
                 const int q = w / TPM;
                 int rb, cb;
                 split_item<MP>(w - q * TPM, RB, CB, rb, cb);
@@ -883,7 +927,12 @@ __global__ void __launch_bounds__(NT) bulk_ptr_kernel(const Params<T> p)
                                                             n, k, p.alpha, p.beta);
             }
         }
-        __syncthreads();
+        if constexpr (DEC) {
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[i % S]);
+        } else {
+            __syncthreads();
+        }
     }
 }
 
