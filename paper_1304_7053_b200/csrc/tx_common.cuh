@@ -42,10 +42,21 @@ __device__ __forceinline__ void mac(float2 &acc, float2 a, float2 b)
     // re += ar*br - (sa*ai)*(sb*bi);  im += ar*(sb*bi) + (sa*ai)*br
     constexpr float sab = (CA != CB) ? 1.f : -1.f;  // -(sa*sb)
     constexpr float sb = CB ? -1.f : 1.f, sa = CA ? -1.f : 1.f;
+#ifndef TX_NO_FFMA2
+    // sm_100 packed fp32 FMA (FFMA2): the same two fmas per component, same operands, same
+    // order (re: ar*br, then (sab*ai)*bi; im: ar*(sb*bi), then (sa*ai)*br), so results are
+    // bitwise those of the scalar chain below, with half the FMA instructions to issue.
+    // ar is a broadcast operand and (bi, br) a half-swap of b, both free in FFMA2; the
+    // signed pair (sab*ai, sa*ai) is built once per a value and reused across the row.
+    const float2 bs = make_float2(sa * sab * b.y, b.x);  // (sa*ai) * bs = (sab*ai*bi, sa*ai*br)
+    acc = __ffma2_rn(make_float2(a.x, a.x), make_float2(b.x, sb * b.y), acc);
+    acc = __ffma2_rn(make_float2(sa * a.y, sa * a.y), bs, acc);
+#else
     acc.x = fmaf(a.x, b.x, acc.x);
     acc.x = fmaf(sab * a.y, b.y, acc.x);
     acc.y = fmaf(a.x, sb * b.y, acc.y);
     acc.y = fmaf(sa * a.y, b.x, acc.y);
+#endif
 }
 template <bool CA, bool CB>
 __device__ __forceinline__ void mac(double2 &acc, double2 a, double2 b)

@@ -107,7 +107,7 @@ def main():
                         finally:
                             tx.set_tuning(0, 0)
                         r = {"kind": kind, "m": m, "n": n, "k": k, "ops": ops, "beta0": not general,
-                             "layout": layout, "tuning": tun, "path": tx.last_path()[0], "jit": tx.last_path_jit(),
+                             "layout": layout, "tuning": tun, "path": tx.last_path()[0], "jit": tx.binding.last_path_jit(),
                              "us": round(t * 1e3, 2),
                              "frac": round(byts / (t / 1e3) / 1e9 / peak, 4), "sets": sets,
                              "tag": a.tag}
