@@ -718,8 +718,19 @@ static int gemm_ptr(char ta, char tb, int m, int n, int k, const U *alpha, const
         // small matrices: 16-byte cp.async chunks over all threads (a per-matrix
         // TMA copy costs ~80 cycles of issue); >= 512-byte matrices: TMA per matrix
         const int min_bytes = es * std::min(m * k, std::min(k * n, m * n));
+        // ... except where the 16-byte gather measured faster on large matrices
+        // (profiles/r02s3_ptr_ab_transA.jsonl): a transposed A without the FP64 tensor cores
+        // (the gather places it swizzled, ASWG; bulk_ptr reads it with bank conflicts):
+        // z 16x3x16 T/C 0.51-0.69 -> 0.61-0.81, d 16x16x16 T/C general 0.53-0.64 -> 0.68-0.77;
+        // c with a C input: 16x16x16 0.50-0.69 -> 0.68-0.80
+        const bool mma = MmaOk<T>::value && (mma_mode() == 1 ||
+                                             (mma_mode() < 0 && mma_jit_rule(AT::cplx, m, n, k, true)));
+        const bool prefer_gather = es == 16 ? (!mma && opa != OP_N)
+                                   : es == 8 && !AT::cplx ? (!b0 && opa != OP_N)
+                                   : es == 8 ? !b0 : false;
         const JitKind kind = !bulk_ok ? JIT_GATHER_PTR
-                                      : (min_bytes >= ptr_bulk_min_bytes() ? JIT_BULK_PTR : JIT_GATHER_PTR16);
+                             : (min_bytes >= ptr_bulk_min_bytes() && !prefer_gather ? JIT_BULK_PTR
+                                                                                    : JIT_GATHER_PTR16);
         e = launch_jit<T>(kind, p, opa, opb, b0, st);
         t_last_path = PATH_PTR | (e == cudaSuccess ? PATH_JIT : 0);
         if (e == cudaErrorNotSupported) e = tab.gather[opa][opb][b0][1](&p, st);

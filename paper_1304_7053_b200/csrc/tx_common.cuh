@@ -42,12 +42,16 @@ __device__ __forceinline__ void mac(float2 &acc, float2 a, float2 b)
     // re += ar*br - (sa*ai)*(sb*bi);  im += ar*(sb*bi) + (sa*ai)*br
     constexpr float sab = (CA != CB) ? 1.f : -1.f;  // -(sa*sb)
     constexpr float sb = CB ? -1.f : 1.f, sa = CA ? -1.f : 1.f;
-#ifndef TX_NO_FFMA2
-    // sm_100 packed fp32 FMA (FFMA2): the same two fmas per component, same operands, same
-    // order (re: ar*br, then (sab*ai)*bi; im: ar*(sb*bi), then (sa*ai)*br), so results are
-    // bitwise those of the scalar chain below, with half the FMA instructions to issue.
-    // ar is a broadcast operand and (bi, br) a half-swap of b, both free in FFMA2; the
-    // signed pair (sab*ai, sa*ai) is built once per a value and reused across the row.
+#ifdef TX_FFMA2
+    // sm_100 packed fp32 FMA (FFMA2; build with -DTX_FFMA2).  An interleaved gate A/B over
+    // all 288 c instances measured no net gain (median ratio 1.002, 79 faster / 68 slower by
+    // > 2 %; profiles/r02s3_ffma2_ab/): ncu (c13 beta = 0) shows issue 69 % -> 56 % but the
+    // FMA pipe 48 % -> 52 % and the same duration -- the kernel is latency / occupancy bound
+    // (16 warps per SM, per-tile barrier), not issue bound.  Kept as an option.
+    // The same two fmas per component, same operand products, same order (re: ar*br, then
+    // (sab*ai)*bi; im: ar*(sb*bi), then (sa*ai)*br; signs moved between factors are exact),
+    // so results are bitwise those of the scalar chain below, with half the FMA instructions;
+    // ar and sa*ai are broadcast operands, free in FFMA2.
     const float2 bs = make_float2(sa * sab * b.y, b.x);  // (sa*ai) * bs = (sab*ai*bi, sa*ai*br)
     acc = __ffma2_rn(make_float2(a.x, a.x), make_float2(b.x, sb * b.y), acc);
     acc = __ffma2_rn(make_float2(sa * a.y, sa * a.y), bs, acc);
