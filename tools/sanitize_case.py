@@ -58,6 +58,25 @@ def main():
             pa, pb, pc = (X.data_ptr() + idx * (s * es) for X, s in ((A, m * k), (B, k * n), (C, m * n)))
             assert tx.tx_gemm_batched_ptr(kind, ta, tb, m, n, k, 0.5, pa, lda, pb, ldb, 0.25, pc, m,
                                           batch) == 0
+    # pointer arrays of 16x16 matrices through bulk_ptr (decoupled ring for d / z general,
+    # per-tile barrier for s general and c beta = 0) with the grid capped at 2 CTAs so every
+    # CTA cycles its stages many times (mbarrier phase flips, empty-barrier waits)
+    if not uninit:
+        prev = tx.set_max_ctas(2)
+        try:
+            for kind, beta in (("d", 0.25), ("z", 0.25), ("s", 0.25), ("c", 0.0)):
+                n, batch = 16, 96
+                e = n * n
+                A = txinputs.values_torch(kind, 7, 0, e * batch, "cuda")
+                B = txinputs.values_torch(kind, 8, 0, e * batch, "cuda")
+                C = txinputs.values_torch(kind, 9, 0, e * batch, "cuda")
+                es = A.element_size()
+                idx = torch.randperm(batch, generator=torch.Generator().manual_seed(5)).cuda()
+                pa, pb, pc = (X.data_ptr() + idx * (e * es) for X in (A, B, C))
+                assert tx.tx_gemm_batched_ptr(kind, "N", "N", n, n, n, 0.5, pa, n, pb, n, beta, pc,
+                                              n, batch) == 0
+        finally:
+            tx.set_max_ctas(prev)
     torch.cuda.synchronize()
     print("ok")
 
