@@ -65,6 +65,15 @@ TypeTables &tables(int t)
 
 static std::atomic<int> g_max_ctas{0};
 int max_ctas_override() { return g_max_ctas.load(std::memory_order_relaxed); }
+// TX_CTAS_PER_SM: cap on resident CTAs per SM for the persistent grids (A/B measurements)
+int ctas_per_sm_cap()
+{
+    static const int v = [] {
+        const char *e = getenv("TX_CTAS_PER_SM");
+        return e && *e ? atoi(e) : 0;
+    }();
+    return v;
+}
 static std::atomic<int> g_tune_stages{0}, g_tune_kb{0};
 int tune_stages() { return g_tune_stages.load(std::memory_order_relaxed); }
 int tune_stage_bytes() { return g_tune_kb.load(std::memory_order_relaxed) * 1024; }

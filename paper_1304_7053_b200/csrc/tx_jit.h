@@ -153,7 +153,9 @@ cudaError_t launch_jit(JitKind kind, Params<T> p, int opa, int opb, bool b0, cud
     p.P = pl.P;
     p.S = pl.S;
     p.ntiles = pl.ntiles;
-    long long grid = (long long)num_sms() * jit_occupancy(f, NT, pl.smem);
+    int occ = jit_occupancy(f, NT, pl.smem);
+    if (ctas_per_sm_cap() > 0 && occ > ctas_per_sm_cap()) occ = ctas_per_sm_cap();
+    long long grid = (long long)num_sms() * occ;
     const int cap = max_ctas_override();
     if (cap > 0 && grid > cap) grid = cap;
     if (grid > pl.ntiles) grid = pl.ntiles;
