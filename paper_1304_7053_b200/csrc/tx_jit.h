@@ -103,13 +103,18 @@ cudaError_t launch_jit(JitKind kind, Params<T> p, int opa, int opb, bool b0, cud
     }();
     // bulk_ptr: two stages of ~16 KB (pointer-array A/B over S x KB, round 2: s16 general
     // 0.54 -> 0.95, z16 beta = 0 0.38 -> 0.85 of HBM against the strided instance's plan)
-    const int kb = gather && gather_kb > 0 ? gather_kb : (kind == JIT_BULK_PTR ? 16 : mp.KB);
+    // strided sizes beyond 16 with a C input: two 32 KB stages (pipeline sweep, round 2,
+    // profiles/r02s3_tune_big.jsonl: s40 general 0.70 -> 0.89, c17 0.65 -> 0.91, c24 0.67 ->
+    // 0.87 of HBM, s24 / s48 / s56 / c28 unchanged within 0.02, s32 0.98 -> 0.96)
+    const bool big_gen = kind == JIT_BULK && !b0 && !bcast && std::max(p.m, std::max(p.n, p.k)) > 16;
+    const int kb = gather && gather_kb > 0 ? gather_kb
+                   : (kind == JIT_BULK_PTR ? 16 : big_gen ? 32 : mp.KB);
     static const bool two_ctas = [] {  // TX_PLAN_2CTA=0: the plain planner (A/B runs)
         const char *v = getenv("TX_PLAN_2CTA");
         return !(v && v[0] == '0');
     }();
     Plan pl = plan_tiles(sizeof(T), p.m, p.n, p.k, b0, mp.RM, mp.RN, NT, p.batch, !gather,
-                         gather ? GS : (kind == JIT_BULK_PTR ? 2 : mp.S), kb, kind == JIT_BULK ? bcast : 0, 0, rows_cap,
+                         gather ? GS : (kind == JIT_BULK_PTR || big_gen ? 2 : mp.S), kb, kind == JIT_BULK ? bcast : 0, 0, rows_cap,
                          kind == JIT_BULK && two_ctas, mma ? 32 * mma_items(cplx, p.m, p.n) : 0);
     if (swz) {
         // the 1024-byte alignment of the swizzled regions: shrink the tile until it fits
