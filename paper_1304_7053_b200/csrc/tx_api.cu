@@ -276,7 +276,12 @@ bool mma_jit_rule(bool cplx, int m, int n, int k, bool ptr)
     // z 1x16x16 0.69 -> 0.91 of HBM and z 16x3x16 0.56 -> 0.92 without, profiles/r02s3_ptr_ab)
     if (ptr && std::min(m, n) < 8) return false;
     const int mx = std::max(m, std::max(n, k));
-    return cplx ? mx >= 13 : mx >= 17;
+    // sizes beyond 16 (DMMA on/off sweep, round 2, profiles/r02s3_big_dmma_ab.jsonl): the
+    // CUDA-core kernel wins for z 17-24 (z17 0.37-0.48 -> 0.78-0.93 of HBM, z20 0.46-0.57 ->
+    // 0.64-0.77, z24 beta = 0 0.59 -> 0.80) and d 33-47 (d40 0.49-0.63 -> 0.75-0.92); DMMA
+    // for z28-32 (0.64-0.85 vs 0.43-0.60) and d17-32 / d48-64
+    if (cplx) return mx >= 13 && (mx <= 16 || mx >= 26);
+    return mx >= 17 && !(mx >= 33 && mx <= 47);
 }
 
 // tcgen05 split-TF32 kernel for s / c (TX_TC=0 never, =1 wherever it applies:
