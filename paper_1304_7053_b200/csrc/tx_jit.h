@@ -107,22 +107,35 @@ cudaError_t launch_jit(JitKind kind, Params<T> p, int opa, int opb, bool b0, cud
     // profiles/r02s3_tune_big.jsonl: s40 general 0.70 -> 0.89, c17 0.65 -> 0.91, c24 0.67 ->
     // 0.87 of HBM, s24 / s48 / s56 / c28 unchanged within 0.02, s32 0.98 -> 0.96)
     const bool big_gen = kind == JIT_BULK && !b0 && !bcast && std::max(p.m, std::max(p.n, p.k)) > 16;
-    // square s with beta = 0 at the sizes where two 16 KB stages measured > 3 % faster than the
-    // modelled plan (profiles/r02s3_sizes17_32.jsonl: 17 0.48 -> 0.73, 21 0.57 -> 0.80,
-    // 23 0.74 -> 0.91, 25 0.44 -> 0.66, 30 0.79 -> 0.94 of HBM; it lost at 19, 20, 24, 32)
-    auto s_b0_two16 = [](int n) {
-        return n == 17 || n == 21 || n == 22 || n == 23 || n == 25 || n == 26 || n == 30;
+    // Square sizes beyond 16: two-stage plans where a pipeline sweep measured them > 3 % faster
+    // than the rule above (stage KB per (type, n, beta = 0); 0 = keep).  s beta = 0:
+    // profiles/r02s3_sizes17_32.jsonl (17 0.48 -> 0.73, 21 0.57 -> 0.80, 25 0.44 -> 0.66, 30 0.79
+    // -> 0.93 of HBM); d / c / z: profiles/r02s3_big_tuning_cdz.jsonl (d19 general 0.84 -> 0.97,
+    // d24 beta = 0 0.86 -> 0.92, c20 general 0.81 -> 0.95, c18 beta = 0 0.81 -> 0.89, z17 beta = 0
+    // 0.74 -> 0.81, z20 beta = 0 0.62 -> 0.68).
+    auto big_kb = [](int es, bool cplx, int n, bool beta0) -> int {
+        if (n < 17 || n > 32) return 0;
+        if (es == 4) return (beta0 && (n == 17 || n == 21 || n == 22 || n == 23 || n == 25 ||
+                                   n == 26 || n == 30)) ? 16 : 0;
+        if (es == 8 && !cplx) {  // d
+            if (beta0) return (n == 17 || n == 18 || n == 20 || n == 22) ? 32
+                          : (n == 19 || n == 21 || n == 23 || n == 24 || n == 27 || n == 28) ? 64 : 0;
+            return (n == 19 || n == 22 || n == 24) ? 64 : 0;
+        }
+        if (es == 8) return beta0 ? (n == 18 ? 16 : 0) : (n == 20 ? 64 : 0);  // c
+        if (beta0) return n <= 22 ? 32 : n <= 25 ? 64 : 0;                     // z
+        return (n == 20 || n == 24) ? 64 : 0;
     };
-    const bool s_b0 = kind == JIT_BULK && b0 && !bcast && sizeof(T) == 4 && p.m == p.n &&
-                      p.n == p.k && s_b0_two16(p.n);
+    const int sq_kb = kind == JIT_BULK && !bcast && p.m == p.n && p.n == p.k
+                          ? big_kb((int)sizeof(T), cplx, p.n, b0) : 0;
     const int kb = gather && gather_kb > 0 ? gather_kb
-                   : (kind == JIT_BULK_PTR || s_b0 ? 16 : big_gen ? 32 : mp.KB);
+                   : (kind == JIT_BULK_PTR ? 16 : sq_kb > 0 ? sq_kb : big_gen ? 32 : mp.KB);
     static const bool two_ctas = [] {  // TX_PLAN_2CTA=0: the plain planner (A/B runs)
         const char *v = getenv("TX_PLAN_2CTA");
         return !(v && v[0] == '0');
     }();
     Plan pl = plan_tiles(sizeof(T), p.m, p.n, p.k, b0, mp.RM, mp.RN, NT, p.batch, !gather,
-                         gather ? GS : (kind == JIT_BULK_PTR || big_gen || s_b0 ? 2 : mp.S), kb, kind == JIT_BULK ? bcast : 0, 0, rows_cap,
+                         gather ? GS : (kind == JIT_BULK_PTR || big_gen || sq_kb > 0 ? 2 : mp.S), kb, kind == JIT_BULK ? bcast : 0, 0, rows_cap,
                          kind == JIT_BULK && two_ctas, mma ? 32 * mma_items(cplx, p.m, p.n) : 0);
     if (swz) {
         // the 1024-byte alignment of the swizzled regions: shrink the tile until it fits
